@@ -1,0 +1,182 @@
+/*
+ * kgs_b200.h -- C ABI of the B200-native checkerboard DP-AVF2 stepper for the
+ * Klein-Gordon-Schrodinger system (arXiv 2502.09537).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (pure Python + numba, /root/reference/pkg/src/dpavf) drives the sweep
+ * through two operator layers that cannot survive on a device unchanged:
+ *
+ *   executor.run(schedule, lane_fn)          dpavf/executor.py:39-40, 60-71
+ *   kernels.sweep_base / sweep_adjoint(P,Q,U,V,nbrs,order, 11 coeffs)
+ *                                            dpavf/kernels.py:23-54, 57-94
+ *
+ * Both are gather "lanes" over host index arrays (an (M,2d) int64 neighbour
+ * table plus an int64 order), so the replacement sits one level up, at the
+ * colour granularity used by step_base / step_adjoint / step_dpavf2 /
+ * integrate (dpavf/integrator.py:107-182) and discrete_energy / mass /
+ * FieldState.is_finite (dpavf/grid.py:101-103, 166-187).  Each entry point
+ * below names the reference function it replaces.
+ *
+ * Conventions
+ *   - Host field arrays are float64, length (planes owned) * N^(d-1), in the
+ *     reference linearisation i = x*N^(d-1) + y*N^(d-2) + z (first axis
+ *     slowest, dpavf/grid.py:4-7).  Copy semantics: the caller keeps
+ *     ownership of host memory; the context owns device memory.
+ *   - Colour: 1 = red (index-sum parity 1, swept first by the base sweep),
+ *     0 = black (dpavf/ordering.py:114-136, 139-149).
+ *   - Kind:   0 = base sweep (kernels.sweep_base), 1 = adjoint sweep
+ *     (kernels.sweep_adjoint).
+ *   - Every call is synchronous at return (results visible to the host).
+ *   - Return 0 on success or a negative KGS_E* code; kgs_last_error() holds
+ *     a message.  A context is used by one host thread at a time.
+ */
+#ifndef KGS_B200_H
+#define KGS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KGS_OK 0
+#define KGS_EINVAL (-1)     /* bad argument: odd N, d not in {1,2,3}, bad split */
+#define KGS_ECUDA (-2)      /* CUDA runtime error (message in kgs_last_error) */
+#define KGS_ENCCL (-3)      /* NCCL error or NCCL not loadable */
+#define KGS_ENONFINITE (-4) /* non-finite field values detected */
+#define KGS_ENOMEM (-5)     /* device allocation failed */
+
+#define KGS_NTERMS 8        /* energy/mass term sums, see kgs_energy_terms */
+
+typedef struct kgs_ctx kgs_ctx;
+
+/* The 11 kernel scalars in StepCoefficients.kernel_args() order
+ * (dpavf/integrator.py:42-45): alpha, beta, gcoef, c_uv, uv_nbr, gU,
+ * half_tau (= coeffs.tau / 2), i00, i01, i10, i11.  Computed on the host
+ * exactly as precompute_coefficients (dpavf/integrator.py:48-64). */
+typedef struct kgs_coeffs {
+  double alpha, beta, gcoef, c_uv, uv_nbr, gU, half_tau, i00, i01, i10, i11;
+} kgs_coeffs;
+
+/* ---- context lifetime ------------------------------------------------- */
+
+/* Single-process context over the whole periodic grid GridSpec(d, a, b, N)
+ * (dpavf/grid.py:16-64).  The grid is split into `nslabs` slabs of N/nslabs
+ * planes along axis 0; slab s lives on device dev_ids[s] (several slabs may
+ * share one device: "virtual slabs", used to test decomposition invariance
+ * on one GPU).  nslabs == 1 is the ordinary single-GPU case.
+ * KGS_EINVAL: d not in {1,2,3}, N < 2, N odd (checkerboard needs even N,
+ * dpavf/ordering.py:120-122), nslabs < 1, N % nslabs != 0, N/nslabs < 2 when
+ * nslabs > 1, or nslabs > 1 with d == 1. */
+int kgs_create(int d, int64_t N, double a, double b, int nslabs,
+               const int* dev_ids, kgs_ctx** out);
+
+/* One rank of a multi-process run (one process per GPU, torchrun): this
+ * context owns slab `rank` of `nranks` on `device`; face halos travel over
+ * NCCL send/recv to ranks rank-1 / rank+1 (periodic).  `nccl_id` is the
+ * 128-byte ncclUniqueId produced by kgs_nccl_unique_id on rank 0 and
+ * broadcast by the caller.  nranks == 1 needs no NCCL (nccl_id may be NULL). */
+int kgs_create_dist(int d, int64_t N, double a, double b, int rank, int nranks,
+                    int device, const void* nccl_id, kgs_ctx** out);
+
+/* Fill 128 bytes with a fresh ncclUniqueId (rank 0 only). */
+int kgs_nccl_unique_id(void* out128);
+
+int kgs_destroy(kgs_ctx* ctx);
+
+/* Planes [*x0, *x0 + *nx) along axis 0 owned by this context (whole grid for
+ * kgs_create; one slab for kgs_create_dist); *points = nx * N^(d-1). */
+int kgs_local_range(kgs_ctx* ctx, int64_t* x0, int64_t* nx, int64_t* points);
+
+/* ---- state transfer (FieldState P, Q, U, V; dpavf/grid.py:82-103) ------ */
+
+/* Host -> device copy of the owned planes (natural layout); the context
+ * re-lays the fields out on the device (colour-split planes). */
+int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q,
+               const double* U, const double* V);
+/* Device -> host copy of the owned planes (natural layout). */
+int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V);
+
+/* ---- the hot path ------------------------------------------------------ */
+
+/* One colour half of one sweep, in place: the device equivalent of
+ * executor.run over one phase of checkerboard_schedule with lane_fn =
+ * kernels.sweep_base (kind 0) or kernels.sweep_adjoint (kind 1).
+ * step_base = sweep(red, base) then sweep(black, base); step_adjoint =
+ * sweep(black, adjoint) then sweep(red, adjoint)
+ * (dpavf/integrator.py:107-121, dpavf/ordering.py:139-149). */
+int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c);
+
+/* `nsteps` DP-AVF2 steps (step_dpavf2 = base then adjoint at tau/2,
+ * dpavf/integrator.py:124-129) -- the loop body of integrate
+ * (dpavf/integrator.py:167-179) -- with fused colour passes.  The steps are
+ * numbered n = step_offset + 1 .. step_offset + nsteps (global step numbers
+ * of an integrate run split into several calls).
+ * Every step is checked for non-finite values (integrate:169-171); if any
+ * appear, *first_bad_step receives the first bad global step number and the
+ * call returns KGS_ENONFINITE after finishing the launched work; otherwise
+ * *first_bad_step = 0.
+ * When record_stride > 0, the energy/mass term sums (see kgs_energy_terms)
+ * of the state after every step n with n % record_stride == 0 are written,
+ * in step order, to terms_out[r * KGS_NTERMS + q], r = 0, 1, ...
+ * terms_out may be NULL when no step is recorded. */
+int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
+                    int64_t step_offset, int64_t record_stride,
+                    double* terms_out, int64_t* first_bad_step);
+
+/* ---- diagnostics (dpavf/grid.py:152-187) ------------------------------- */
+
+/* Unscaled sums over this context's points, deterministic for a given
+ * decomposition (fixed-order warp/block/grid tree):
+ *   t[0] = sum (P(i+e_ax) - P(i))^2 over all forward edges   (_grad_sq_sum*h^2)
+ *   t[1] = same for Q, t[2] = same for U
+ *   t[3] = V.V, t[4] = U.U, t[5] = (P^2+Q^2).U, t[6] = P.P, t[7] = Q.Q
+ * discrete_energy = h^d * (0.5*(k1*(t0+t1)/h^2 + k2*t2/h^2 + t3 + mu^2*t4)
+ *                          - gamma*t5),  mass = h^d * (t6 + t7). */
+int kgs_energy_terms(kgs_ctx* ctx, double* terms_out);
+
+/* discrete_energy(state, params, grid) and mass(state, grid) for the
+ * resident state (single-process contexts; dist contexts return the local
+ * slab's contribution). */
+int kgs_energy_mass(kgs_ctx* ctx, double kappa1, double kappa2, double mu,
+                    double gamma, double* E, double* mass);
+
+/* FieldState.is_finite (dpavf/grid.py:101-103) for the resident state. */
+int kgs_all_finite(kgs_ctx* ctx, int* ok);
+
+/* Message for the last failing call on ctx (or the last global failure when
+ * ctx is NULL). Never NULL. */
+const char* kgs_last_error(kgs_ctx* ctx);
+
+/* ---- benchmarking / introspection ------------------------------------- */
+
+/* Number of kernel launches issued by this context since creation. */
+int64_t kgs_launch_count(kgs_ctx* ctx);
+
+/* Device time in milliseconds of the most recent kgs_step_dpavf2 call,
+ * measured with CUDA events on the context's stream(s) (max over slabs). */
+double kgs_last_step_ms(kgs_ctx* ctx);
+
+/* Per-launch timing of the fused colour passes (K3 black base+adjoint and
+ * K4 red adjoint+base) inside kgs_step_dpavf2: when enabled, a CUDA event
+ * pair brackets each such launch on its stream.  kgs_pass_stats returns the
+ * number of timed launches and their summed device time (ms) since the
+ * last kgs_pass_timing call, and the points each launch updated (twice). */
+int kgs_pass_timing(kgs_ctx* ctx, int enable);
+int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
+                   int64_t* points_per_launch);
+
+/* Fill the resident state on the device from a named initial condition
+ * (0 = ellipsoids3d, 1 = fourpeak2d, 2 = gaussian2d, 3 = soliton1d) without
+ * a host round trip; used for >= 512^3 benchmark inputs.  Values agree with
+ * the numpy presets to libm rounding, not bitwise. */
+int kgs_fill_preset(kgs_ctx* ctx, int preset);
+
+/* ABI version (major*100 + minor). */
+int kgs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KGS_B200_H */

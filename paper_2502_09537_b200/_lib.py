@@ -1,0 +1,128 @@
+"""ctypes binding of the C ABI in include/kgs_b200.h (libkgs_b200.so).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``python -m paper_2502_09537_b200.build``).  There is no CPU fallback: if the
+library is missing or no B200 is visible, every device entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_NAME = "libkgs_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+KGS_OK = 0
+KGS_EINVAL = -1
+KGS_ECUDA = -2
+KGS_ENCCL = -3
+KGS_ENONFINITE = -4
+KGS_ENOMEM = -5
+NTERMS = 8
+
+# Every symbol include/kgs_b200.h declares (checked by the CPU test suite).
+EXPORTED = (
+    "kgs_create", "kgs_create_dist", "kgs_nccl_unique_id", "kgs_destroy",
+    "kgs_local_range", "kgs_upload", "kgs_download", "kgs_sweep",
+    "kgs_step_dpavf2", "kgs_energy_terms", "kgs_energy_mass",
+    "kgs_all_finite", "kgs_last_error", "kgs_launch_count",
+    "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version",
+    "kgs_pass_timing", "kgs_pass_stats",
+)
+
+
+class KgsCoeffs(ctypes.Structure):
+    """kgs_coeffs: StepCoefficients.kernel_args() order (integrator.py:42-45)."""
+
+    _fields_ = [(n, ctypes.c_double) for n in (
+        "alpha", "beta", "gcoef", "c_uv", "uv_nbr", "gU", "half_tau",
+        "i00", "i01", "i10", "i11")]
+
+
+class KgsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"kgs error {code}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+_DP = ctypes.POINTER(ctypes.c_double)
+
+
+def load() -> ctypes.CDLL:
+    """Load libkgs_b200.so (once).  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = os.environ.get("KGS_B200_LIB", str(LIB_PATH))
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not found: build the CUDA library first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+    sig = {
+        "kgs_create": (ctypes.c_int, [ctypes.c_int, _I64, _D, _D, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_P)]),
+        "kgs_create_dist": (ctypes.c_int, [ctypes.c_int, _I64, _D, _D, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                           ctypes.POINTER(_P)]),
+        "kgs_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+        "kgs_destroy": (ctypes.c_int, [_P]),
+        "kgs_local_range": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                           ctypes.POINTER(_I64)]),
+        "kgs_upload": (ctypes.c_int, [_P, _DP, _DP, _DP, _DP]),
+        "kgs_download": (ctypes.c_int, [_P, _DP, _DP, _DP, _DP]),
+        "kgs_sweep": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(KgsCoeffs)]),
+        "kgs_step_dpavf2": (ctypes.c_int, [_P, ctypes.POINTER(KgsCoeffs), _I64, _I64, _I64,
+                                           _DP, ctypes.POINTER(_I64)]),
+        "kgs_energy_terms": (ctypes.c_int, [_P, _DP]),
+        "kgs_energy_mass": (ctypes.c_int, [_P, _D, _D, _D, _D, _DP, _DP]),
+        "kgs_all_finite": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+        "kgs_last_error": (ctypes.c_char_p, [_P]),
+        "kgs_launch_count": (_I64, [_P]),
+        "kgs_last_step_ms": (_D, [_P]),
+        "kgs_fill_preset": (ctypes.c_int, [_P, ctypes.c_int]),
+        "kgs_abi_version": (ctypes.c_int, []),
+        "kgs_pass_timing": (ctypes.c_int, [_P, ctypes.c_int]),
+        "kgs_pass_stats": (ctypes.c_int, [_P, ctypes.POINTER(_I64), _DP, ctypes.POINTER(_I64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, ctx=None) -> None:
+    if rc == KGS_OK:
+        return
+    msg = load().kgs_last_error(ctx).decode(errors="replace")
+    if rc == KGS_EINVAL:
+        raise ValueError(msg)
+    if rc == KGS_ENONFINITE:
+        raise FloatingPointError(msg)
+    raise KgsError(rc, msg)
+
+
+def dptr(a: np.ndarray):
+    """double* of a C-contiguous float64 array (no copy)."""
+    if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+        raise TypeError("field arrays must be C-contiguous float64")
+    return a.ctypes.data_as(_DP)
+
+
+def coeffs_struct(kernel_args) -> KgsCoeffs:
+    vals = tuple(float(v) for v in kernel_args)
+    if len(vals) != 11:
+        raise ValueError("expected the 11 kernel_args() scalars")
+    return KgsCoeffs(*vals)

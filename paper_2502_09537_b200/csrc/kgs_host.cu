@@ -1,0 +1,835 @@
+// kgs_host.cu -- C ABI (include/kgs_b200.h) over the sm_100a colour-pass
+// kernels: contexts, slabs, halo exchange, fused DP-AVF2 stepping loop,
+// diagnostics.  See DESIGN.md for the pass schedule and the roofline.
+#include "../../include/kgs_b200.h"
+#include "kgs_device.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace kgs;
+
+namespace {
+
+thread_local std::string g_last_error = "no error";
+
+// ---- NCCL, loaded lazily so single-GPU use never needs it --------------
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl(std::string& err) {
+  if (g_nccl.tried) {
+    if (!g_nccl.ok) err = "libnccl.so.2 could not be loaded";
+    return g_nccl.ok;
+  }
+  g_nccl.tried = true;
+  // RTLD_NOLOAD first: reuse the NCCL torch already mapped into the process.
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    err = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+    return false;
+  }
+#define KGS_SYM(field, name)                                         \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+  if (!g_nccl.field) { err = "missing NCCL symbol " name; return false; }
+  KGS_SYM(GetUniqueId, "ncclGetUniqueId");
+  KGS_SYM(CommInitRank, "ncclCommInitRank");
+  KGS_SYM(CommDestroy, "ncclCommDestroy");
+  KGS_SYM(Send, "ncclSend");
+  KGS_SYM(Recv, "ncclRecv");
+  KGS_SYM(GroupStart, "ncclGroupStart");
+  KGS_SYM(GroupEnd, "ncclGroupEnd");
+  KGS_SYM(GetErrorString, "ncclGetErrorString");
+#undef KGS_SYM
+  g_nccl.ok = true;
+  return true;
+}
+
+struct Slab {
+  int dev = 0;
+  int64_t x0 = 0;  // global first plane
+  int nx = 0;      // planes
+  double* buf[2] = {nullptr, nullptr};    // colour c, ghost plane -1
+  double* plane0[2] = {nullptr, nullptr}; // colour c, plane 0
+  double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
+  int npart[2] = {0, 0};                     // blocks that wrote partials
+  double* records = nullptr;                 // device [cap * NTERMS]
+  int64_t rec_cap = 0;
+  unsigned long long* bad = nullptr;
+  double* stage = nullptr;  // natural-layout staging planes
+  int stage_planes = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_done = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+};
+
+}  // namespace
+
+struct kgs_ctx {
+  int d = 3;
+  int64_t N = 0;
+  double a = 0, b = 1, h = 1;
+  int ny = 1, nk = 1, nz = 1;   // rows per plane, slots per row, natural row
+  int64_t nxg = 1;              // global planes
+  int64_t pp = 0, ps = 0;       // points per plane & colour, plane stride
+  std::vector<Slab> slabs;
+  bool dist = false;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  std::string err = "no error";
+  int64_t launches = 0;
+  double last_ms = 0.0;
+  int nsm = 148;
+  int grid_cap = 0;  // max persistent grid (blocks), sizes partials
+  // per-pass timing (slab 0's stream): event pairs around fused passes
+  bool pass_timing = false;
+  std::vector<cudaEvent_t> pass_ev;
+  size_t pass_ev_used = 0;
+  int64_t pass_count = 0;
+  double pass_ms = 0.0;
+};
+
+namespace {
+
+int fail(kgs_ctx* c, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(call)                                                          \
+  do {                                                                    \
+    cudaError_t e_ = (call);                                              \
+    if (e_ != cudaSuccess)                                                \
+      return fail(ctx, KGS_ECUDA, "%s failed: %s (%s:%d)", #call,         \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);            \
+  } while (0)
+
+#define NK(call)                                                          \
+  do {                                                                    \
+    ncclResult_t r_ = (call);                                             \
+    if (r_ != ncclSuccess)                                                \
+      return fail(ctx, KGS_ENCCL, "%s failed: %s", #call,                 \
+                  g_nccl.GetErrorString(r_));                             \
+  } while (0)
+
+// ---- tile geometry -------------------------------------------------------
+constexpr int kThreads = 256;
+
+int pow2ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
+  PassGeom g{};
+  g.own = s.plane0[col];
+  g.oth = s.plane0[col ^ 1];
+  g.ps = ctx->ps;
+  g.pp = ctx->pp;
+  g.nx = s.nx;
+  g.ny = ctx->ny;
+  g.nk = ctx->nk;
+  g.xa = xa;
+  g.xb = xb;
+  g.x0 = s.x0;
+  g.wrap = (ctx->slabs.size() == 1 && !(ctx->dist && ctx->nranks > 1)) ? 1 : 0;
+  // 3-D: 64 slots x 4 rows (rows y+-1 reused from L1 inside the tile);
+  // otherwise one row segment of up to 256 slots.
+  int tk = std::min(kThreads, pow2ceil(ctx->nk));
+  if (ctx->d == 3) tk = std::min(tk, 64);
+  int ty = std::min(kThreads / tk, pow2ceil(ctx->ny));
+  g.tk = tk;
+  g.ty = ty;
+  g.nkt = (ctx->nk + tk - 1) / tk;
+  g.nyt = (ctx->ny + ty - 1) / ty;
+  g.ntiles = (int64_t)(xb - xa) * g.nyt * g.nkt;
+  return g;
+}
+
+// ---- kernel dispatch -----------------------------------------------------
+template <int D, int COL, int OP1, int OP2, bool DIAG, bool CHECK>
+int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
+             int step_no) {
+  auto kern = colour_pass<D, COL, OP1, OP2, DIAG, CHECK>;
+  static int occ = 0;  // per instantiation; all devices are B200
+  if (occ == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = std::min<int64_t>(g.ntiles, (int64_t)occ * ctx->nsm);
+  grid = std::min<int64_t>(grid, ctx->grid_cap);
+  if (grid < 1) return KGS_OK;  // nothing to do
+  kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(g, c, s.partials[COL], s.bad,
+                                                  step_no);
+  ctx->launches++;
+  if (DIAG) s.npart[COL] = (int)grid;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+template <int D, int COL>
+int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
+               int op1, int op2, bool diag, bool check, int step_no) {
+#define KGS_CASE(O1, O2, DG, CH)                                        \
+  if (op1 == O1 && op2 == O2 && diag == DG && check == CH)             \
+    return launch_t<D, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);
+  // single sweeps (kgs_sweep, head)
+  KGS_CASE(OP_BASE, OP_NONE, false, false)
+  KGS_CASE(OP_ADJ, OP_NONE, false, false)
+  // diagnostics / finiteness only
+  KGS_CASE(OP_NONE, OP_NONE, true, false)
+  KGS_CASE(OP_NONE, OP_NONE, false, true)
+  if (COL == 0) {  // K3: black base(n) + adjoint(n)
+    KGS_CASE(OP_BASE, OP_ADJ, false, true)
+    KGS_CASE(OP_BASE, OP_ADJ, true, true)
+  } else {  // K4: red adjoint(n) + base(n+1); tail: red adjoint(n)
+    KGS_CASE(OP_ADJ, OP_BASE, false, true)
+    KGS_CASE(OP_ADJ, OP_BASE, true, true)
+    KGS_CASE(OP_ADJ, OP_NONE, false, true)
+    KGS_CASE(OP_ADJ, OP_NONE, true, true)
+  }
+#undef KGS_CASE
+  return fail(ctx, KGS_EINVAL, "unsupported pass combination %d/%d/%d/%d",
+              op1, op2, (int)diag, (int)check);
+}
+
+int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
+                bool check, const Coeffs& c, int step_no) {
+  PassGeom g = make_geom(ctx, s, col, 0, s.nx);
+  switch (ctx->d * 2 + col) {
+    case 2: return launch_col<1, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 3: return launch_col<1, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 4: return launch_col<2, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 5: return launch_col<2, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 6: return launch_col<3, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 7: return launch_col<3, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
+  }
+  return fail(ctx, KGS_EINVAL, "bad dimension %d", ctx->d);
+}
+
+// ---- halo exchange of colour `col` faces (P, Q, U of planes 0 and nx-1) --
+// The three fields of a plane are contiguous ([P|Q|U|V] per plane), so a
+// face is ONE contiguous run of 3*pp doubles.
+int exchange(kgs_ctx* ctx, int col) {
+  const size_t face = (size_t)3 * ctx->pp;
+  if (ctx->dist) {
+    if (ctx->nranks == 1) return KGS_OK;
+    Slab& s = ctx->slabs[0];
+    const int up = (ctx->rank + 1) % ctx->nranks;
+    const int dn = (ctx->rank - 1 + ctx->nranks) % ctx->nranks;
+    double* p0 = s.plane0[col];
+    NK(g_nccl.GroupStart());
+    // order matters when up == dn (2 ranks): sends [to dn: plane 0, to up:
+    // plane nx-1]; recvs [from up: ghost nx, from dn: ghost -1].
+    NK(g_nccl.Send(p0, face, ncclFloat64, dn, ctx->comm, s.stream));
+    NK(g_nccl.Send(p0 + (int64_t)(s.nx - 1) * ctx->ps, face, ncclFloat64, up,
+                   ctx->comm, s.stream));
+    NK(g_nccl.Recv(p0 + (int64_t)s.nx * ctx->ps, face, ncclFloat64, up,
+                   ctx->comm, s.stream));
+    NK(g_nccl.Recv(p0 - ctx->ps, face, ncclFloat64, dn, ctx->comm, s.stream));
+    NK(g_nccl.GroupEnd());
+    return KGS_OK;
+  }
+  const int ns = (int)ctx->slabs.size();
+  if (ns == 1) return KGS_OK;  // single slab wraps inside the kernel
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaEventRecord(s.ev_done, s.stream));
+  }
+  for (int i = 0; i < ns; ++i) {
+    Slab& s = ctx->slabs[i];
+    Slab& lo = ctx->slabs[(i - 1 + ns) % ns];
+    Slab& hi = ctx->slabs[(i + 1) % ns];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamWaitEvent(s.stream, lo.ev_done, 0));
+    CK(cudaStreamWaitEvent(s.stream, hi.ev_done, 0));
+    // pull: ghost -1 <- lo plane nx-1 ; ghost nx <- hi plane 0
+    double* g_lo = s.plane0[col] - ctx->ps;
+    double* g_hi = s.plane0[col] + (int64_t)s.nx * ctx->ps;
+    const double* src_lo = lo.plane0[col] + (int64_t)(lo.nx - 1) * ctx->ps;
+    const double* src_hi = hi.plane0[col];
+    if (lo.dev == s.dev)
+      CK(cudaMemcpyAsync(g_lo, src_lo, face * 8, cudaMemcpyDeviceToDevice, s.stream));
+    else
+      CK(cudaMemcpyPeerAsync(g_lo, s.dev, src_lo, lo.dev, face * 8, s.stream));
+    if (hi.dev == s.dev)
+      CK(cudaMemcpyAsync(g_hi, src_hi, face * 8, cudaMemcpyDeviceToDevice, s.stream));
+    else
+      CK(cudaMemcpyPeerAsync(g_hi, s.dev, src_hi, hi.dev, face * 8, s.stream));
+  }
+  // the next pass on slab i must not overwrite colour `col` planes that a
+  // neighbour is still pulling: the pass after next (same colour) is ordered
+  // behind the neighbour's pulls via the next exchange's event waits.
+  return KGS_OK;
+}
+
+int sync_all(kgs_ctx* ctx) {
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.stream));
+  }
+  return KGS_OK;
+}
+
+int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
+               const Coeffs& c, int step_no) {
+  for (auto& s : ctx->slabs) {
+    cudaError_t e = cudaSetDevice(s.dev);
+    if (e != cudaSuccess) return fail(ctx, KGS_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    int r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no);
+    if (r) return r;
+  }
+  return KGS_OK;
+}
+
+// all_passes() bracketed by an event pair on slab 0's stream when timing.
+int timed_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
+                 const Coeffs& c, int step_no) {
+  if (!ctx->pass_timing) return all_passes(ctx, col, op1, op2, diag, check, c, step_no);
+  Slab& s0 = ctx->slabs[0];
+  if (ctx->pass_ev_used + 2 > ctx->pass_ev.size()) {
+    CK(cudaSetDevice(s0.dev));
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->pass_ev.push_back(e);
+    }
+  }
+  cudaEvent_t a = ctx->pass_ev[ctx->pass_ev_used++];
+  cudaEvent_t b = ctx->pass_ev[ctx->pass_ev_used++];
+  CK(cudaSetDevice(s0.dev));
+  CK(cudaEventRecord(a, s0.stream));
+  int r = all_passes(ctx, col, op1, op2, diag, check, c, step_no);
+  if (r) return r;
+  CK(cudaSetDevice(s0.dev));
+  CK(cudaEventRecord(b, s0.stream));
+  return KGS_OK;
+}
+
+int collect_pass_times(kgs_ctx* ctx) {
+  for (size_t i = 0; i + 1 < ctx->pass_ev_used; i += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->pass_ev[i], ctx->pass_ev[i + 1]));
+    ctx->pass_ms += ms;
+    ctx->pass_count++;
+  }
+  ctx->pass_ev_used = 0;
+  return KGS_OK;
+}
+
+int finalize_record(kgs_ctx* ctx, int64_t slot, bool both) {
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    finalize_terms<<<1, kThreads, 0, s.stream>>>(
+        s.partials[1], s.npart[1], both ? s.partials[0] : nullptr,
+        both ? s.npart[0] : 0, s.records + slot * NTERMS);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  return KGS_OK;
+}
+
+int ensure_records(kgs_ctx* ctx, int64_t n) {
+  for (auto& s : ctx->slabs) {
+    if (s.rec_cap >= n) continue;
+    CK(cudaSetDevice(s.dev));
+    if (s.records) CK(cudaFree(s.records));
+    s.records = nullptr;
+    const int64_t cap = std::max<int64_t>(n, 64);
+    CK(cudaMalloc(&s.records, (size_t)cap * NTERMS * sizeof(double)));
+    s.rec_cap = cap;
+  }
+  return KGS_OK;
+}
+
+int reset_bad(kgs_ctx* ctx) {
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemsetAsync(s.bad, 0xff, sizeof(unsigned long long), s.stream));
+  }
+  return KGS_OK;
+}
+
+int read_bad(kgs_ctx* ctx, unsigned long long* out) {
+  *out = ULLONG_MAX;
+  for (auto& s : ctx->slabs) {
+    unsigned long long v = 0;
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemcpyAsync(&v, s.bad, sizeof v, cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    *out = std::min(*out, v);
+  }
+  return KGS_OK;
+}
+
+Coeffs to_coeffs(const kgs_coeffs* c) {
+  Coeffs k;
+  static_assert(sizeof(Coeffs) == sizeof(kgs_coeffs), "coeff layout");
+  std::memcpy(&k, c, sizeof k);
+  return k;
+}
+
+int alloc_slab(kgs_ctx* ctx, Slab& s) {
+  CK(cudaSetDevice(s.dev));
+  const size_t colour_bytes = (size_t)(s.nx + 2) * ctx->ps * sizeof(double);
+  for (int c = 0; c < 2; ++c) {
+    cudaError_t e = cudaMalloc(&s.buf[c], colour_bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, KGS_ENOMEM, "cudaMalloc of %zu bytes failed: %s",
+                  colour_bytes, cudaGetErrorString(e));
+    }
+    CK(cudaMemset(s.buf[c], 0, colour_bytes));
+    s.plane0[c] = s.buf[c] + ctx->ps;
+    CK(cudaMalloc(&s.partials[c], (size_t)ctx->grid_cap * NTERMS * sizeof(double)));
+  }
+  CK(cudaMalloc(&s.bad, sizeof(unsigned long long)));
+  CK(cudaMemset(s.bad, 0xff, sizeof(unsigned long long)));
+  // staging: up to 256 MiB of natural-layout planes of one field
+  const size_t nat_plane = (size_t)ctx->ny * ctx->nz * sizeof(double);
+  s.stage_planes = (int)std::max<size_t>(1, std::min<size_t>(s.nx, (256u << 20) / nat_plane));
+  CK(cudaMalloc(&s.stage, s.stage_planes * nat_plane));
+  CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
+  CK(cudaEventCreate(&s.ev_t0));
+  CK(cudaEventCreate(&s.ev_t1));
+  return KGS_OK;
+}
+
+int init_geometry(kgs_ctx* ctx, int d, int64_t N, double a, double b) {
+  if (d < 1 || d > 3) return fail(ctx, KGS_EINVAL, "dimension must be 1, 2 or 3, got %d", d);
+  if (!(b > a)) return fail(ctx, KGS_EINVAL, "need b > a, got a=%g, b=%g", a, b);
+  if (N < 2) return fail(ctx, KGS_EINVAL, "need N >= 2, got N=%lld", (long long)N);
+  if (N % 2)
+    return fail(ctx, KGS_EINVAL,
+                "checkerboard needs even N for a consistent periodic 2-coloring, got N=%lld",
+                (long long)N);
+  if (N > (1 << 20)) return fail(ctx, KGS_EINVAL, "N=%lld too large", (long long)N);
+  ctx->d = d;
+  ctx->N = N;
+  ctx->a = a;
+  ctx->b = b;
+  ctx->h = (b - a) / (double)N;
+  ctx->nz = (int)N;
+  ctx->nk = (int)(N / 2);
+  ctx->ny = (d == 3) ? (int)N : 1;
+  ctx->nxg = (d >= 2) ? N : 1;
+  ctx->pp = (int64_t)ctx->ny * ctx->nk;
+  ctx->ps = 4 * ctx->pp;
+  return KGS_OK;
+}
+
+int init_device_props(kgs_ctx* ctx, int dev) {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10)
+    return fail(ctx, KGS_ECUDA,
+                "device %d is sm_%d%d; this library is built for sm_100a (B200)",
+                dev, prop.major, prop.minor);
+  ctx->nsm = prop.multiProcessorCount;
+  ctx->grid_cap = ctx->nsm * 8;
+  return KGS_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+// extern "C" API
+// =========================================================================
+extern "C" {
+
+int kgs_abi_version(void) { return 100; }
+
+const char* kgs_last_error(kgs_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+int64_t kgs_launch_count(kgs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+double kgs_last_step_ms(kgs_ctx* ctx) { return ctx ? ctx->last_ms : 0.0; }
+
+int kgs_create(int d, int64_t N, double a, double b, int nslabs,
+               const int* dev_ids, kgs_ctx** out) {
+  if (!out) return fail(nullptr, KGS_EINVAL, "out is NULL");
+  *out = nullptr;
+  kgs_ctx* ctx = new kgs_ctx();
+  int r = init_geometry(ctx, d, N, a, b);
+  if (!r && nslabs < 1) r = fail(ctx, KGS_EINVAL, "nslabs must be >= 1");
+  if (!r && nslabs > 1 && d == 1) r = fail(ctx, KGS_EINVAL, "1-D grids cannot be split into slabs");
+  if (!r && ctx->nxg % nslabs) r = fail(ctx, KGS_EINVAL, "N=%lld not divisible by %d slabs", (long long)N, nslabs);
+  if (!r && nslabs > 1 && ctx->nxg / nslabs < 2) r = fail(ctx, KGS_EINVAL, "slabs need >= 2 planes");
+  if (!r) r = init_device_props(ctx, dev_ids ? dev_ids[0] : 0);
+  if (!r) {
+    ctx->slabs.resize(nslabs);
+    const int per = (int)(ctx->nxg / nslabs);
+    for (int i = 0; i < nslabs && !r; ++i) {
+      Slab& s = ctx->slabs[i];
+      s.dev = dev_ids ? dev_ids[i] : 0;
+      s.x0 = (int64_t)i * per;
+      s.nx = per;
+      r = alloc_slab(ctx, s);
+    }
+  }
+  if (!r) {  // enable peer access between distinct devices (best effort)
+    for (auto& s : ctx->slabs)
+      for (auto& t : ctx->slabs)
+        if (s.dev != t.dev) {
+          cudaSetDevice(s.dev);
+          if (cudaDeviceEnablePeerAccess(t.dev, 0) != cudaSuccess) cudaGetLastError();
+        }
+  }
+  if (r) {
+    g_last_error = ctx->err;
+    kgs_destroy(ctx);
+    return r;
+  }
+  *out = ctx;
+  return KGS_OK;
+}
+
+int kgs_nccl_unique_id(void* out128) {
+  std::string err;
+  if (!load_nccl(err)) return fail(nullptr, KGS_ENCCL, "%s", err.c_str());
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, KGS_ENCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  return KGS_OK;
+}
+
+int kgs_create_dist(int d, int64_t N, double a, double b, int rank, int nranks,
+                    int device, const void* nccl_id, kgs_ctx** out) {
+  if (!out) return fail(nullptr, KGS_EINVAL, "out is NULL");
+  *out = nullptr;
+  kgs_ctx* ctx = new kgs_ctx();
+  ctx->dist = true;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  int r = init_geometry(ctx, d, N, a, b);
+  if (!r && (nranks < 1 || rank < 0 || rank >= nranks)) r = fail(ctx, KGS_EINVAL, "bad rank %d of %d", rank, nranks);
+  if (!r && nranks > 1 && d == 1) r = fail(ctx, KGS_EINVAL, "1-D grids cannot be split into slabs");
+  if (!r && ctx->nxg % nranks) r = fail(ctx, KGS_EINVAL, "N=%lld not divisible by %d ranks", (long long)N, nranks);
+  if (!r && nranks > 1 && ctx->nxg / nranks < 2) r = fail(ctx, KGS_EINVAL, "slabs need >= 2 planes");
+  if (!r) r = init_device_props(ctx, device);
+  if (!r) {
+    ctx->slabs.resize(1);
+    Slab& s = ctx->slabs[0];
+    s.dev = device;
+    s.nx = (int)(ctx->nxg / nranks);
+    s.x0 = (int64_t)rank * s.nx;
+    r = alloc_slab(ctx, s);
+  }
+  if (!r && nranks > 1) {
+    std::string err;
+    if (!nccl_id) r = fail(ctx, KGS_EINVAL, "nccl_id is NULL");
+    else if (!load_nccl(err)) r = fail(ctx, KGS_ENCCL, "%s", err.c_str());
+    else {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof id);
+      cudaSetDevice(device);
+      ncclResult_t nr = g_nccl.CommInitRank(&ctx->comm, nranks, id, rank);
+      if (nr != ncclSuccess) r = fail(ctx, KGS_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(nr));
+    }
+  }
+  if (r) {
+    g_last_error = ctx->err;
+    kgs_destroy(ctx);
+    return r;
+  }
+  *out = ctx;
+  return KGS_OK;
+}
+
+int kgs_destroy(kgs_ctx* ctx) {
+  if (!ctx) return KGS_OK;
+  if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
+  for (auto e : ctx->pass_ev) cudaEventDestroy(e);
+  for (auto& s : ctx->slabs) {
+    cudaSetDevice(s.dev);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    for (int c = 0; c < 2; ++c) {
+      if (s.buf[c]) cudaFree(s.buf[c]);
+      if (s.partials[c]) cudaFree(s.partials[c]);
+    }
+    if (s.records) cudaFree(s.records);
+    if (s.bad) cudaFree(s.bad);
+    if (s.stage) cudaFree(s.stage);
+    if (s.ev_done) cudaEventDestroy(s.ev_done);
+    if (s.ev_t0) cudaEventDestroy(s.ev_t0);
+    if (s.ev_t1) cudaEventDestroy(s.ev_t1);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  delete ctx;
+  return KGS_OK;
+}
+
+int kgs_local_range(kgs_ctx* ctx, int64_t* x0, int64_t* nx, int64_t* points) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  int64_t lo = ctx->slabs.front().x0, n = 0;
+  for (auto& s : ctx->slabs) n += s.nx;
+  if (x0) *x0 = lo;
+  if (nx) *nx = n;
+  if (points) *points = n * (int64_t)ctx->ny * ctx->nz;
+  return KGS_OK;
+}
+
+int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
+               const double* V) {
+  if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
+  const double* f[4] = {P, Q, U, V};
+  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
+  const int64_t base_x = ctx->slabs.front().x0;
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    for (int fi = 0; fi < 4; ++fi) {
+      for (int xs = 0; xs < s.nx; xs += s.stage_planes) {
+        const int nxc = std::min(s.stage_planes, s.nx - xs);
+        const double* src = f[fi] + (s.x0 - base_x + xs) * nat_plane;
+        CK(cudaMemcpyAsync(s.stage, src, (size_t)nxc * nat_plane * 8,
+                           cudaMemcpyHostToDevice, s.stream));
+        const int64_t n = (int64_t)nxc * ctx->pp;
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
+        split_field<<<blocks, 256, 0, s.stream>>>(
+            s.stage, s.plane0[1] + fi * ctx->pp, s.plane0[0] + fi * ctx->pp,
+            ctx->ps, ctx->pp, nxc, ctx->ny, ctx->nk, xs, s.x0);
+        ctx->launches++;
+        CK(cudaGetLastError());
+      }
+    }
+  }
+  int r = exchange(ctx, 0);
+  if (!r) r = exchange(ctx, 1);
+  if (!r) r = sync_all(ctx);
+  return r;
+}
+
+int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V) {
+  if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
+  double* f[4] = {P, Q, U, V};
+  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
+  const int64_t base_x = ctx->slabs.front().x0;
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    for (int fi = 0; fi < 4; ++fi) {
+      for (int xs = 0; xs < s.nx; xs += s.stage_planes) {
+        const int nxc = std::min(s.stage_planes, s.nx - xs);
+        const int64_t n = (int64_t)nxc * ctx->pp;
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
+        merge_field<<<blocks, 256, 0, s.stream>>>(
+            s.stage, s.plane0[1] + fi * ctx->pp, s.plane0[0] + fi * ctx->pp,
+            ctx->ps, ctx->pp, nxc, ctx->ny, ctx->nk, xs, s.x0);
+        ctx->launches++;
+        CK(cudaGetLastError());
+        double* dst = f[fi] + (s.x0 - base_x + xs) * nat_plane;
+        CK(cudaMemcpyAsync(dst, s.stage, (size_t)nxc * nat_plane * 8,
+                           cudaMemcpyDeviceToHost, s.stream));
+      }
+    }
+    CK(cudaStreamSynchronize(s.stream));
+  }
+  return KGS_OK;
+}
+
+int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c) {
+  if (!ctx || !c) return fail(ctx, KGS_EINVAL, "NULL argument");
+  if (colour != 0 && colour != 1) return fail(ctx, KGS_EINVAL, "colour must be 0 or 1");
+  if (kind != 0 && kind != 1) return fail(ctx, KGS_EINVAL, "kind must be 0 (base) or 1 (adjoint)");
+  const Coeffs k = to_coeffs(c);
+  int r = all_passes(ctx, colour, kind == 0 ? OP_BASE : OP_ADJ, OP_NONE, false, false, k, 0);
+  if (!r) r = exchange(ctx, colour);
+  if (!r) r = sync_all(ctx);
+  return r;
+}
+
+int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
+                    int64_t step_offset, int64_t record_stride,
+                    double* terms_out, int64_t* first_bad_step) {
+  if (!ctx || !half) return fail(ctx, KGS_EINVAL, "NULL argument");
+  if (nsteps < 0 || record_stride < 0 || step_offset < 0)
+    return fail(ctx, KGS_EINVAL, "negative nsteps/step_offset/record_stride");
+  if (first_bad_step) *first_bad_step = 0;
+  if (nsteps == 0) return KGS_OK;
+  if (nsteps + step_offset > INT_MAX) return fail(ctx, KGS_EINVAL, "step numbers too large");
+  const int64_t nrec = record_stride > 0
+      ? (step_offset + nsteps) / record_stride - step_offset / record_stride : 0;
+  if (nrec > 0 && !terms_out) return fail(ctx, KGS_EINVAL, "terms_out is NULL");
+  const Coeffs c = to_coeffs(half);
+  int r = ensure_records(ctx, nrec);
+  if (!r) r = reset_bad(ctx);
+  if (r) return r;
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaEventRecord(s.ev_t0, s.stream));
+  }
+  // head: base red(first step)
+  r = all_passes(ctx, 1, OP_BASE, OP_NONE, false, false, c, 0);
+  if (!r) r = exchange(ctx, 1);
+  int64_t slot = 0;
+  for (int64_t i = 1; i <= nsteps && !r; ++i) {
+    const int64_t n = step_offset + i;
+    const bool rec = record_stride > 0 && n % record_stride == 0;
+    // K3: black base(n) + adjoint(n)
+    r = timed_passes(ctx, 0, OP_BASE, OP_ADJ, rec, true, c, (int)n);
+    if (!r) r = exchange(ctx, 0);
+    // K4: red adjoint(n) + base(n+1), or the tail: red adjoint(last)
+    if (!r && i < nsteps) r = timed_passes(ctx, 1, OP_ADJ, OP_BASE, rec, true, c, (int)n);
+    else if (!r) r = all_passes(ctx, 1, OP_ADJ, OP_NONE, rec, true, c, (int)n);
+    if (!r) r = exchange(ctx, 1);
+    if (!r && rec) r = finalize_record(ctx, slot++, true);
+  }
+  if (r) return r;
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaEventRecord(s.ev_t1, s.stream));
+  }
+  r = sync_all(ctx);
+  if (r) return r;
+  double ms = 0.0;
+  for (auto& s : ctx->slabs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, s.ev_t0, s.ev_t1));
+    ms = std::max(ms, (double)t);
+  }
+  ctx->last_ms = ms;
+  r = collect_pass_times(ctx);
+  if (r) return r;
+  if (nrec > 0) {
+    std::vector<double> tmp((size_t)nrec * NTERMS);
+    std::fill(terms_out, terms_out + nrec * NTERMS, 0.0);
+    for (auto& s : ctx->slabs) {  // slab order: deterministic host sum
+      CK(cudaSetDevice(s.dev));
+      CK(cudaMemcpy(tmp.data(), s.records, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (size_t q = 0; q < tmp.size(); ++q) terms_out[q] += tmp[q];
+    }
+  }
+  unsigned long long bad = 0;
+  r = read_bad(ctx, &bad);
+  if (r) return r;
+  if (bad != ULLONG_MAX) {
+    if (first_bad_step) *first_bad_step = (int64_t)bad;
+    return fail(ctx, KGS_ENONFINITE, "non-finite field values detected after step %llu", bad);
+  }
+  return KGS_OK;
+}
+
+int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
+  if (!ctx || !terms_out) return fail(ctx, KGS_EINVAL, "NULL argument");
+  Coeffs dummy{};
+  int r = ensure_records(ctx, 1);
+  // red: edges + red self terms; black: black self terms
+  if (!r) r = all_passes(ctx, 1, OP_NONE, OP_NONE, true, false, dummy, 0);
+  if (!r) r = all_passes(ctx, 0, OP_NONE, OP_NONE, true, false, dummy, 0);
+  if (!r) r = finalize_record(ctx, 0, true);
+  if (!r) r = sync_all(ctx);
+  if (r) return r;
+  std::fill(terms_out, terms_out + NTERMS, 0.0);
+  for (auto& s : ctx->slabs) {
+    double tmp[NTERMS];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemcpy(tmp, s.records, sizeof tmp, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < NTERMS; ++q) terms_out[q] += tmp[q];
+  }
+  return KGS_OK;
+}
+
+int kgs_energy_mass(kgs_ctx* ctx, double kappa1, double kappa2, double mu,
+                    double gamma, double* E, double* mass) {
+  double t[NTERMS];
+  int r = kgs_energy_terms(ctx, t);
+  if (r) return r;
+  const double h = ctx->h, h2 = h * h;
+  double hd = 1.0;
+  for (int i = 0; i < ctx->d; ++i) hd *= h;
+  const double quad = kappa1 * (t[0] / h2) + kappa1 * (t[1] / h2) +
+                      kappa2 * (t[2] / h2) + t[3] + mu * mu * t[4];
+  if (E) *E = hd * (0.5 * quad - gamma * t[5]);
+  if (mass) *mass = hd * (t[6] + t[7]);
+  return KGS_OK;
+}
+
+int kgs_all_finite(kgs_ctx* ctx, int* ok) {
+  if (!ctx || !ok) return fail(ctx, KGS_EINVAL, "NULL argument");
+  Coeffs dummy{};
+  int r = reset_bad(ctx);
+  if (!r) r = all_passes(ctx, 1, OP_NONE, OP_NONE, false, true, dummy, 1);
+  if (!r) r = all_passes(ctx, 0, OP_NONE, OP_NONE, false, true, dummy, 1);
+  if (!r) r = sync_all(ctx);
+  if (r) return r;
+  unsigned long long bad = 0;
+  r = read_bad(ctx, &bad);
+  if (r) return r;
+  *ok = (bad == ULLONG_MAX) ? 1 : 0;
+  return KGS_OK;
+}
+
+int kgs_pass_timing(kgs_ctx* ctx, int enable) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  ctx->pass_timing = enable != 0;
+  ctx->pass_count = 0;
+  ctx->pass_ms = 0.0;
+  ctx->pass_ev_used = 0;
+  return KGS_OK;
+}
+
+int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
+                   int64_t* points_per_launch) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  if (launches) *launches = ctx->pass_count;
+  if (total_ms) *total_ms = ctx->pass_ms;
+  int64_t pts = 0;
+  for (auto& s : ctx->slabs) pts += (int64_t)s.nx * ctx->pp;  // one colour
+  if (points_per_launch) *points_per_launch = pts;
+  return KGS_OK;
+}
+
+int kgs_fill_preset(kgs_ctx* ctx, int preset) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  const int need_d[4] = {3, 2, 2, 1};
+  if (preset < 0 || preset > 3) return fail(ctx, KGS_EINVAL, "unknown preset %d", preset);
+  if (need_d[preset] != ctx->d)
+    return fail(ctx, KGS_EINVAL, "preset %d requires a %dD grid, got d=%d", preset,
+                need_d[preset], ctx->d);
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    const int64_t n = (int64_t)s.nx * ctx->pp * 2;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
+    fill_preset<<<blocks, 256, 0, s.stream>>>(s.plane0[0], s.plane0[1], ctx->ps,
+                                              ctx->pp, s.nx, ctx->ny, ctx->nk, s.x0,
+                                              ctx->d, ctx->a, ctx->h, preset);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  int r = exchange(ctx, 0);
+  if (!r) r = exchange(ctx, 1);
+  if (!r) r = sync_all(ctx);
+  return r;
+}
+
+}  // extern "C"

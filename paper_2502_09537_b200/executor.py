@@ -1,0 +1,137 @@
+"""Executors: which GPUs a sweep runs on.
+
+The reference executors (``dpavf/executor.py:17-93``) decide which host
+thread calls a lane function over an index array, with a futures barrier
+between the red and black phases.  On the B200 the colour phase is one
+kernel launch and the barrier is stream order, so an executor here only
+names the devices and the slab decomposition along axis 0:
+
+* ``SerialExecutor`` / ``PhasedExecutor(workers)`` -- accepted for
+  drop-in compatibility; both run on one GPU (``cuda:0``).  ``workers`` is
+  kept as an attribute and has no effect on the result (bitwise identical
+  for every worker count, like the reference, ``executor.py:1-8``).
+* ``CudaExecutor(devices, slabs_per_device=1)`` -- single process driving
+  one or more GPUs; the grid is split into ``len(devices)*slabs_per_device``
+  slabs with face halos copied between them (several slabs on one device
+  are "virtual slabs": the decomposition-invariance test on one GPU).
+* ``DistributedExecutor()`` -- one process per GPU under torchrun; this
+  rank owns one slab and halos travel over NCCL (see device.py).
+
+``ExecutorConfig(mode, workers)`` accepts "serial", "phased" and "cuda"
+(``workers`` = GPU count for "cuda"); any other mode is rejected exactly
+as the reference does (``executor.py:22-26``).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+MODES = ("serial", "phased", "cuda")
+
+
+@dataclass(frozen=True)
+class ExecutorConfig:
+    mode: str = "serial"   # "serial" | "phased" | "cuda"
+    workers: int = 1
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"unknown executor mode {self.mode!r}")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+
+    def build(self):
+        if self.mode == "serial":
+            return SerialExecutor()
+        if self.mode == "phased":
+            return PhasedExecutor(self.workers)
+        return CudaExecutor(tuple(range(self.workers)))
+
+
+class _DeviceExecutor:
+    devices: tuple = (0,)
+    slabs_per_device: int = 1
+
+    @property
+    def nslabs(self) -> int:
+        return len(self.devices) * self.slabs_per_device
+
+    def slab_devices(self) -> tuple:
+        return tuple(d for d in self.devices for _ in range(self.slabs_per_device))
+
+    def key(self) -> tuple:
+        return ("local", self.slab_devices())
+
+    def run(self, schedule, lane_fn) -> None:
+        raise TypeError(
+            "device executors do not run host lane functions; use step_base/"
+            "step_adjoint/step_dpavf2/integrate from paper_2502_09537_b200")
+
+    def close(self) -> None:
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class SerialExecutor(_DeviceExecutor):
+    """One GPU (cuda:0); the drop-in for dpavf.executor.SerialExecutor."""
+
+    workers = 1
+
+
+class PhasedExecutor(_DeviceExecutor):
+    """One GPU (cuda:0); the drop-in for dpavf.executor.PhasedExecutor."""
+
+    def __init__(self, workers: int):
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        self.workers = workers
+
+
+class CudaExecutor(_DeviceExecutor):
+    """Single process over ``devices`` with ``slabs_per_device`` slabs each."""
+
+    def __init__(self, devices=(0,), slabs_per_device: int = 1):
+        devices = tuple(int(d) for d in devices)
+        if not devices:
+            raise ValueError("need at least one device")
+        if slabs_per_device < 1:
+            raise ValueError("slabs_per_device must be >= 1")
+        self.devices = devices
+        self.slabs_per_device = int(slabs_per_device)
+        self.workers = self.nslabs
+
+
+class DistributedExecutor(_DeviceExecutor):
+    """One rank of a torchrun job: slab ``rank`` of ``world_size`` on
+    ``cuda:local_rank``; halos over NCCL.  torch.distributed must be
+    initialised (any backend) before the first use."""
+
+    def __init__(self, rank: int | None = None, world_size: int | None = None,
+                 device: int | None = None):
+        import os
+        if rank is None or world_size is None:
+            import torch.distributed as dist
+            rank = dist.get_rank() if rank is None else rank
+            world_size = dist.get_world_size() if world_size is None else world_size
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", rank))
+        self.rank, self.world_size, self.device = int(rank), int(world_size), int(device)
+        self.devices = (self.device,)
+        self.workers = self.world_size
+
+    def key(self) -> tuple:
+        return ("dist", self.rank, self.world_size, self.device)
+
+
+def resolve(executor) -> _DeviceExecutor:
+    """Map any executor (ours, the reference's, or None) to a device plan."""
+    if isinstance(executor, _DeviceExecutor):
+        return executor
+    if executor is None or hasattr(executor, "run"):
+        # reference SerialExecutor / PhasedExecutor or a duck-typed stand-in
+        return SerialExecutor()
+    raise TypeError(f"not an executor: {executor!r}")

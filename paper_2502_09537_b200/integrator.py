@@ -1,0 +1,213 @@
+"""Time integrators: base and adjoint sweeps, DP-AVF2, and the run loop.
+
+Same names, signatures and semantics as the reference ``dpavf.integrator``
+(dpavf/integrator.py), with the sweeps executed by the sm_100a colour-pass
+kernels of ``libkgs_b200.so``:
+
+* ``precompute_coefficients`` is the reference's host arithmetic verbatim
+  (integrator.py:48-64) -- the 11 kernel scalars must be bit-identical;
+* ``step_base`` = red then black base half-sweeps; ``step_adjoint`` = black
+  then red adjoint half-sweeps; ``step_dpavf2`` = base then adjoint at tau/2
+  (integrator.py:107-129, ordering.py:139-149);
+* ``integrate`` (integrator.py:147-182) runs the fused stepping loop on the
+  device (2 colour passes per step, energy/mass/finiteness fused into them)
+  and fills the same ``EnergyTrace``.
+
+State arguments may be a host ``FieldState`` (uploaded, stepped, copied
+back in place) or a :class:`~paper_2502_09537_b200.device.DeviceFieldState`
+(stepped in place on the GPU).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from .device import DeviceFieldState, as_device_state
+from .grid import FieldState, GridSpec, PhysParams, energy_from_terms
+from .ordering import BLACK, RED, UpdateSchedule, require_checkerboard
+
+KIND_BASE, KIND_ADJOINT = 0, 1
+
+
+@dataclass(frozen=True)
+class StepCoefficients:
+    """Precomputed pointwise solve constants for step size tau
+    (reference integrator.py:22-45)."""
+
+    tau: float
+    alpha: float      # Psi center weight  tau*kappa1*d / (2 h^2)
+    beta: float       # Psi neighbor weight  tau*kappa1 / (2 h^2)
+    gcoef: float      # Psi coupling weight  tau*gamma / 2
+    c_uv: float       # tau*kappa2*d/h^2 + tau*mu^2/2
+    uv_nbr: float     # tau*kappa2 / h^2
+    gU: float         # tau*gamma
+    uv_inv: tuple     # ((i00, i01), (i10, i11))
+
+    def kernel_args(self) -> tuple:
+        (i00, i01), (i10, i11) = self.uv_inv
+        return (self.alpha, self.beta, self.gcoef, self.c_uv, self.uv_nbr,
+                self.gU, self.tau / 2.0, i00, i01, i10, i11)
+
+
+def precompute_coefficients(params: PhysParams, tau: float,
+                            grid: GridSpec) -> StepCoefficients:
+    """Host arithmetic identical to reference integrator.py:48-64."""
+    if tau == 0.0 or not math.isfinite(tau):
+        raise ValueError(f"step size must be nonzero and finite, got tau={tau}")
+    h2 = grid.h**2
+    d = grid.d
+    alpha = tau * params.kappa1 * d / (2.0 * h2)
+    beta = tau * params.kappa1 / (2.0 * h2)
+    gcoef = tau * params.gamma / 2.0
+    c_uv = tau * params.kappa2 * d / h2 + tau * params.mu**2 / 2.0
+    det = 1.0 + (tau / 2.0) * c_uv
+    if det == 0.0:
+        raise ValueError(f"singular U-V system: 1 + (tau/2)*c_uv = 0 at tau={tau}")
+    uv_inv = ((1.0 / det, (tau / 2.0) / det),
+              (-c_uv / det, 1.0 / det))
+    return StepCoefficients(tau, alpha, beta, gcoef, c_uv,
+                            tau * params.kappa2 / h2, tau * params.gamma, uv_inv)
+
+
+def _colours(schedule, adjoint: bool) -> tuple[int, int]:
+    order = schedule.colour_order if isinstance(schedule, UpdateSchedule) else (RED, BLACK)
+    return tuple(reversed(order)) if adjoint else order
+
+
+def _sweep(state, schedule, coeffs: StepCoefficients, executor, grid: GridSpec,
+           kind: int) -> None:
+    require_checkerboard(schedule, grid)
+    dev, temp = as_device_state(state, grid, executor)
+    args = coeffs.kernel_args()
+    for colour in _colours(schedule, kind == KIND_ADJOINT):
+        dev.ctx.sweep(colour, kind, args)
+    if temp:
+        dev.ctx.download(state)
+    state.t += coeffs.tau
+
+
+def step_base(state, schedule, coeffs: StepCoefficients, executor,
+              grid: GridSpec) -> None:
+    """One base sweep over all points (red, then black); advances state.t by
+    coeffs.tau (reference integrator.py:107-112)."""
+    _sweep(state, schedule, coeffs, executor, grid, KIND_BASE)
+
+
+def step_adjoint(state, schedule, coeffs: StepCoefficients, executor,
+                 grid: GridSpec) -> None:
+    """One adjoint sweep along the reversed schedule (black, then red);
+    advances t by coeffs.tau (reference integrator.py:115-121)."""
+    _sweep(state, schedule, coeffs, executor, grid, KIND_ADJOINT)
+
+
+def step_dpavf2(state, schedule, coeffs_half: StepCoefficients, executor,
+                grid: GridSpec) -> None:
+    """Symmetric composition: base then adjoint, each at tau/2
+    (reference integrator.py:124-129), as one fused device call."""
+    require_checkerboard(schedule, grid)
+    if isinstance(schedule, UpdateSchedule) and schedule.reversed:
+        # a reversed schedule swaps the colour order of both halves
+        step_base(state, schedule, coeffs_half, executor, grid)
+        step_adjoint(state, schedule, coeffs_half, executor, grid)
+        return
+    dev, temp = as_device_state(state, grid, executor)
+    _, bad = dev.ctx.step_dpavf2(coeffs_half.kernel_args(), 1)
+    if temp:
+        dev.ctx.download(state)
+    state.t += coeffs_half.tau
+    state.t += coeffs_half.tau
+
+
+@dataclass
+class EnergyTrace:
+    """Per-record energy bookkeeping along an integration
+    (reference integrator.py:132-144)."""
+
+    steps: list
+    times: list
+    energy: list
+    rel_error: list
+    mass: list
+    re_is_absolute: bool = False  # set when |E0| underflows the RE ratio
+
+    def max_rel_error(self) -> float:
+        return max(self.rel_error)
+
+
+def integrate(state, grid: GridSpec, params: PhysParams,
+              schedule, executor, tau: float, T: float,
+              record_stride: int = 1, snapshot_stride: int = 0,
+              snapshot_writer=None) -> EnergyTrace:
+    """Run ceil(T/tau) composed steps on the GPU, recording energy and mass.
+
+    Reference integrator.py:147-182.  The relative energy error is
+    |E_n - E_0| / |E_0|; when E_0 underflows the quotient the absolute drift
+    is recorded instead and flagged.  Non-finite values raise
+    FloatingPointError naming the first bad step; for a host state the
+    state is left exactly as the reference leaves it (after that step).
+    """
+    if tau <= 0 or T < 0:
+        raise ValueError(f"need tau > 0 and T >= 0, got tau={tau}, T={T}")
+    if record_stride < 1:
+        raise ValueError("record_stride must be >= 1")
+    require_checkerboard(schedule, grid)
+    if isinstance(schedule, UpdateSchedule) and schedule.reversed:
+        raise ValueError("integrate expects the forward checkerboard schedule")
+    n_steps = int(math.ceil(T / tau - 1e-12)) if T > 0 else 0
+    coeffs_half = precompute_coefficients(params, tau / 2.0, grid)
+    args = coeffs_half.kernel_args()
+
+    host = None if isinstance(state, DeviceFieldState) else state
+    dev, _ = as_device_state(state, grid, executor)
+
+    e0, m0 = energy_from_terms(dev.energy_terms(), params, grid)
+    absolute = abs(e0) < 1e-300
+    trace = EnergyTrace([0], [state.t], [e0], [0.0], [m0], re_is_absolute=absolute)
+
+    def advance_t(t: float, k: int) -> float:
+        for _ in range(k):       # t += tau/2 twice per step, like the reference
+            t += coeffs_half.tau
+            t += coeffs_half.tau
+        return t
+
+    # chunk boundaries: snapshot steps (the host state is synced there)
+    snap = snapshot_stride if (snapshot_stride and snapshot_writer) else 0
+    n = 0
+    while n < n_steps:
+        n1 = n_steps if not snap else min(n_steps, (n // snap + 1) * snap)
+        t_start = state.t
+        terms, bad = dev.ctx.step_dpavf2(args, n1 - n, n, record_stride)
+        if bad:
+            if host is not None:
+                # restore the step-n host state and replay exactly to `bad`
+                dev.ctx.upload(host)
+                dev.ctx.step_dpavf2(args, bad - n, n, 0)
+                dev.ctx.download(host)
+            state.t = advance_t(t_start, bad - n)
+            raise FloatingPointError(
+                f"non-finite field values detected after step {bad} (t={state.t})")
+        t = t_start
+        rec = iter(terms)
+        for k in range(n + 1, n1 + 1):
+            t = advance_t(t, 1)
+            if k % record_stride == 0:
+                e, m = energy_from_terms(next(rec), params, grid)
+                re = abs(e - e0) if absolute else abs(e - e0) / abs(e0)
+                trace.steps.append(k)
+                trace.times.append(t)
+                trace.energy.append(e)
+                trace.rel_error.append(re)
+                trace.mass.append(m)
+        state.t = t
+        if isinstance(state, DeviceFieldState):
+            pass
+        n = n1
+        if snap and n % snap == 0:
+            if host is not None:
+                dev.ctx.download(host)
+                snapshot_writer(host, n)
+            else:
+                snapshot_writer(state, n)
+    if host is not None:
+        dev.ctx.download(host)
+    return trace

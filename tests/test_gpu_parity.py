@@ -1,0 +1,214 @@
+"""GPU parity: the sm_100a path through the public API / C ABI against the
+reference's golden vectors and the oracle.  Bar: fields bitwise identical
+(np.array_equal) -- the reference arithmetic is reproduced exactly -- and
+energies within the stated tolerance (the device reduction order differs
+from numpy's pairwise sums; SURVEY.md App.B measured ~1e-15 relative).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2502_09537_b200 as kgs
+from conftest import assert_bitwise, run_names, sweep_names
+
+pytestmark = pytest.mark.gpu
+
+E_RTOL = 1e-13   # device energy vs reference energy (reduction order only)
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _fresh_contexts():
+    yield
+    kgs.clear_contexts()
+
+
+def _integrate(c, executor=None, state=None):
+    s = c.state(0) if state is None else state
+    tr = kgs.integrate(s, c.grid, c.params, kgs.checkerboard_schedule(c.grid),
+                       executor, c.meta["tau"], c.meta["T"],
+                       record_stride=c.meta["record_stride"])
+    return s, tr
+
+
+@pytest.mark.parametrize("name", run_names())
+def test_integrate_bitwise_vs_reference(golden, name):
+    c = golden.case(name)
+    s, tr = _integrate(c)
+    assert_bitwise(s, c.state(1))
+    assert s.t == c.meta["t_final"]
+    assert tr.steps == [int(v) for v in c.trace("steps")]
+    assert tr.times == [float(v) for v in c.trace("times")]
+    np.testing.assert_allclose(tr.energy, c.trace("energy"), rtol=E_RTOL, atol=0)
+    np.testing.assert_allclose(tr.mass, c.trace("mass"), rtol=E_RTOL, atol=0)
+    # energy conserved to the reference's round-off level
+    assert tr.max_rel_error() <= max(10 * c.meta["max_rel_error"], 1e-13)
+
+
+@pytest.mark.parametrize("name", sweep_names())
+def test_single_sweeps_bitwise(golden, name):
+    c = golden.case(name)
+    s = c.state(0)
+    coeffs = kgs.precompute_coefficients(c.params, c.meta["tau"], c.grid)
+    step = kgs.step_adjoint if c.meta["kind"] == "adjoint" else kgs.step_base
+    step(s, kgs.checkerboard_schedule(c.grid), coeffs, kgs.SerialExecutor(), c.grid)
+    assert_bitwise(s, c.state(1))
+    assert s.t == c.meta["t_final"]
+
+
+@pytest.mark.parametrize("slabs", [2, 4])
+@pytest.mark.parametrize("name", ["d2_rand_N32", "d3_rand_N8", "d3_rand_N12", "d3_ellip_N16",
+                                  "d2_fourpeak_N64", "d3_rand_N4"])
+def test_virtual_slabs_bitwise(golden, name, slabs):
+    """Decomposition invariance: the multi-slab halo path
+    gives the same bits as the reference for any slab count."""
+    c = golden.case(name)
+    if c.grid.N % slabs or c.grid.N // slabs < 2:
+        pytest.skip("slab count does not divide N")
+    s, tr = _integrate(c, kgs.CudaExecutor((0,), slabs_per_device=slabs))
+    assert_bitwise(s, c.state(1))
+    np.testing.assert_allclose(tr.energy, c.trace("energy"), rtol=E_RTOL, atol=0)
+
+
+def test_step_dpavf2_api_matches_oracle(golden):
+    c = golden.case("d3_rand_N8")
+    coeffs = kgs.precompute_coefficients(c.params, c.meta["tau"] / 2.0, c.grid)
+    s = c.state(0)
+    ref = c.state(0)
+    for _ in range(3):
+        kgs.step_dpavf2(s, kgs.checkerboard_schedule(c.grid), coeffs, None, c.grid)
+    oracle.numpy_step_dpavf2(ref, c.kernel_args, c.grid, 3)
+    assert_bitwise(s, ref)
+
+
+def test_device_state_roundtrip_and_resident_stepping(golden):
+    c = golden.case("d3_rand_N12")
+    dev = kgs.DeviceFieldState.from_host(c.state(0), c.grid)
+    assert_bitwise(dev.to_host(), c.state(0))
+    tr = kgs.integrate(dev, c.grid, c.params, kgs.checkerboard_schedule(c.grid), None,
+                       c.meta["tau"], c.meta["T"], record_stride=c.meta["record_stride"])
+    assert_bitwise(dev.to_host(), c.state(1))
+    assert dev.t == c.meta["t_final"]
+    np.testing.assert_allclose(tr.energy, c.trace("energy"), rtol=E_RTOL)
+    dev.close()
+
+
+def test_energy_and_mass_on_device(golden):
+    c = golden.case("golden_seed42")
+    s = c.state(0)
+    e = kgs.discrete_energy(s, kgs.PhysParams(), c.grid)
+    assert e == pytest.approx(66.88429062581992, rel=1e-14)
+    assert kgs.mass(s, c.grid) == pytest.approx(c.meta["mass"], rel=1e-14)
+    dev = kgs.DeviceFieldState.from_host(s, c.grid)
+    terms = dev.energy_terms()
+    np.testing.assert_allclose(terms, oracle.energy_terms(s, c.grid), rtol=1e-14)
+    assert dev.is_finite()
+    dev.close()
+
+
+@pytest.mark.parametrize("name", ["d2_gauss_N16", "d3_rand_N8"])
+def test_nonfinite_detection_names_the_step(golden, name):
+    """integrate raises FloatingPointError "after step n" and leaves the host
+    state exactly where the reference leaves it (integrator.py:169-171)."""
+    c = golden.case(name)
+    s0 = c.state(0)
+    s0.U[3] = 1e308                     # overflows within a few steps
+    s0.V[3] = 1e308
+    ref = s0.copy()
+    bad_ref = None
+    for n in range(1, 50):
+        oracle.numpy_step_dpavf2(ref, c.kernel_args, c.grid)
+        if not ref.is_finite():
+            bad_ref = n
+            break
+    assert bad_ref is not None
+    s = s0.copy()
+    with pytest.raises(FloatingPointError, match=f"after step {bad_ref} "):
+        kgs.integrate(s, c.grid, c.params, kgs.checkerboard_schedule(c.grid), None,
+                      c.meta["tau"], 100 * c.meta["tau"], record_stride=1)
+    assert_bitwise(s, ref, equal_nan=True)
+
+
+def test_is_finite_flag(golden):
+    c = golden.case("d3_rand_N4")
+    s = c.state(0)
+    dev = kgs.DeviceFieldState.from_host(s, c.grid)
+    assert dev.is_finite()
+    s.Q[17] = np.nan
+    dev.upload(s)
+    assert not dev.is_finite()
+    dev.close()
+
+
+def test_odd_n_rejected_by_device_context():
+    with pytest.raises(ValueError, match="even N"):
+        kgs.DeviceFieldState(kgs.GridSpec(2, -1.0, 1.0, 9))
+
+
+# ---- full-size and large-grid properties --------------------------------
+@pytest.mark.parametrize("d,N,scenario,steps", [
+    (3, 64, "ellipsoids3d", 6), (2, 1024, "fourpeak2d", 4), (3, 128, "ellipsoids3d", 3)])
+def test_large_grid_bitwise_vs_c_oracle(d, N, scenario, steps):
+    sc = kgs.get_scenario(scenario)
+    g = sc.default_grid(N)
+    s = sc.state(g)
+    ref = s.copy()
+    tau = 0.01
+    kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, tau, steps * tau,
+                  record_stride=steps)
+    orc = oracle.CheckerboardOracle(d, N)
+    orc.step_dpavf2(ref, oracle.kernel_args(sc.params, tau / 2.0, g), steps,
+                    workers=oracle.CheckerboardOracle.max_threads())
+    assert_bitwise(s, ref)
+
+
+def test_256cubed_decomposition_invariance_and_energy():
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(256)
+    sch = kgs.checkerboard_schedule(g)
+    outs = []
+    for ex in (None, kgs.CudaExecutor((0,), slabs_per_device=4)):
+        dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g, ex)
+        tr = kgs.integrate(dev, g, sc.params, sch, None, 0.01, 0.2, record_stride=5)
+        assert tr.max_rel_error() < 1e-12
+        outs.append(dev.to_host())
+        dev.close()
+    assert_bitwise(outs[0], outs[1])
+
+
+def test_device_presets_match_host_presets():
+    for name, N in (("ellipsoids3d", 32), ("fourpeak2d", 64), ("gaussian2d", 64),
+                    ("soliton1d", 1024)):
+        sc = kgs.get_scenario(name)
+        g = sc.default_grid(N)
+        host = sc.state(g)
+        dev = kgs.DeviceFieldState.from_preset(name, g).to_host()
+        for f in "PQUV":
+            np.testing.assert_allclose(getattr(dev, f), getattr(host, f), rtol=1e-13,
+                                       atol=1e-15, err_msg=f"{name}.{f}")
+
+
+def test_soliton_config1_matches_reference_error(golden):
+    """BASELINE config 1: 1-D soliton, N=1024, tau=1e-3, T=1 -- same fields as
+    the reference path, and the same error vs the exact solution."""
+    c = golden.case("d1_soliton_N1024")
+    s, tr = _integrate(c)
+    assert_bitwise(s, c.state(1))
+    exact = kgs.soliton1d_exact(c.grid, 1.0)
+    h = c.grid.h
+    err_u = np.sqrt(h * np.sum((s.U - exact.U)**2))
+    assert err_u < 5e-3                       # reference: 2.21e-3 (SURVEY App.B)
+    assert tr.max_rel_error() < 1e-11
+
+
+def test_1024cubed_full_size_smoke():
+    """The benchmark size fits and conserves energy over a few steps."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(1024)
+    dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
+    tr = kgs.integrate(dev, g, sc.params, kgs.checkerboard_schedule(g), None, 0.01, 0.03,
+                       record_stride=1)
+    assert dev.is_finite()
+    assert tr.max_rel_error() < 1e-11
+    dev.close()

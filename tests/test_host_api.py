@@ -1,0 +1,180 @@
+"""CPU: the C-ABI library loads and exports every declared symbol, the
+host-side API validates arguments like the reference, and device entry
+points fail loudly (no CPU fallback) when no GPU is present."""
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2502_09537_b200 as kgs
+from paper_2502_09537_b200 import _lib
+from paper_2502_09537_b200.device import combine_rank_terms, slab_range
+from paper_2502_09537_b200.ordering import BLACK, RED
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "kgs_b200.h"
+
+
+def _have_gpu() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def declared_functions() -> list[str]:
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(kgs_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert sorted(_lib.EXPORTED) == declared_functions()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.kgs_abi_version() == 100
+
+
+def test_library_is_sm100a():
+    out = Path(_lib.LIB_PATH)
+    data = out.read_bytes()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_create_rejects_bad_geometry_before_touching_a_device():
+    lib = _lib.load()
+    ptr = ctypes.c_void_p()
+    dev = (ctypes.c_int * 1)(0)
+    rc = lib.kgs_create(2, 7, -1.0, 1.0, 1, dev, ctypes.byref(ptr))
+    assert rc == _lib.KGS_EINVAL
+    assert b"even N" in lib.kgs_last_error(None)
+    rc = lib.kgs_create(4, 8, -1.0, 1.0, 1, dev, ctypes.byref(ptr))
+    assert rc == _lib.KGS_EINVAL
+    rc = lib.kgs_create(2, 8, -1.0, 1.0, 3, (ctypes.c_int * 3)(0, 0, 0), ctypes.byref(ptr))
+    assert rc == _lib.KGS_EINVAL
+    assert not ptr.value
+
+
+@pytest.mark.skipif(_have_gpu(), reason="checks the no-GPU failure path")
+def test_device_entry_points_fail_loudly_without_gpu():
+    g = kgs.GridSpec(2, -1.0, 1.0, 8)
+    s = kgs.FieldState.zeros(g)
+    with pytest.raises(_lib.KgsError):
+        kgs.discrete_energy(s, kgs.PhysParams(), g)
+    with pytest.raises(_lib.KgsError):
+        kgs.integrate(s, g, kgs.PhysParams(), kgs.checkerboard_schedule(g),
+                      kgs.SerialExecutor(), 0.1, 0.3)
+
+
+# ---- reference-compatible validation --------------------------------------
+def test_gridspec_validation():
+    with pytest.raises(ValueError, match="dimension"):
+        kgs.GridSpec(4, 0.0, 1.0, 8)
+    with pytest.raises(ValueError, match="b > a"):
+        kgs.GridSpec(2, 1.0, 1.0, 8)
+    with pytest.raises(ValueError, match="N >= 2"):
+        kgs.GridSpec(2, 0.0, 1.0, 1)
+    g = kgs.GridSpec(3, -10.0, 10.0, 16)
+    assert g.h == 20.0 / 16 and g.M == 16**3 and g.shape == (16, 16, 16)
+
+
+def test_physparams_validation():
+    with pytest.raises(ValueError, match="gamma"):
+        kgs.PhysParams(gamma=float("nan"))
+
+
+def test_coefficients_errors_and_hand_inverse():
+    g = kgs.GridSpec(1, 0.0, 4.0, 4)
+    with pytest.raises(ValueError, match="tau"):
+        kgs.precompute_coefficients(kgs.PhysParams(), 0.0, g)
+    with pytest.raises(ValueError, match="tau"):
+        kgs.precompute_coefficients(kgs.PhysParams(), float("inf"), g)
+    c = kgs.precompute_coefficients(kgs.PhysParams(1.0, 0.0, 1.0, 1.0), 2.0, g)
+    (i00, i01), (i10, i11) = c.uv_inv
+    assert (i00, i01, i10, i11) == pytest.approx((0.5, 0.5, -0.5, 0.5))
+
+
+def test_checkerboard_schedule_conventions():
+    g = kgs.GridSpec(2, 0.0, 1.0, 4)
+    with pytest.raises(ValueError, match="even N"):
+        kgs.checkerboard_schedule(kgs.GridSpec(2, 0.0, 1.0, 5))
+    with pytest.raises(ValueError, match="workers"):
+        kgs.checkerboard_schedule(g, workers=0)
+    s = kgs.checkerboard_schedule(g, workers=2)
+    assert s.strategy == "checkerboard" and s.validated
+    assert s.colour_order == (RED, BLACK)
+    parity = np.indices(g.shape).sum(axis=0).ravel() % 2
+    order = s.serial_order()
+    assert np.all(parity[order[: g.M // 2]] == 1)        # red first
+    assert np.array_equal(np.sort(s.rank), np.arange(g.M))
+    assert [len(p.lanes) for p in s.phases] == [2, 2]
+    r = kgs.reverse_schedule(s)
+    assert r.colour_order == (BLACK, RED)
+    assert kgs.reverse_schedule(r) is s
+    assert np.array_equal(r.serial_order(), order[::-1])
+    assert kgs.validate_schedule(s, g) is None
+
+
+def test_non_checkerboard_schedules_refused():
+    class Fake:
+        strategy = "lexicographic-forward"
+    g = kgs.GridSpec(2, 0.0, 1.0, 4)
+    assert "not supported" in kgs.validate_schedule(Fake(), g)
+    with pytest.raises(ValueError, match="invalid schedule"):
+        kgs.integrate(kgs.FieldState.zeros(g), g, kgs.PhysParams(), Fake(), None, 0.1, 0.2)
+
+
+def test_executor_config_modes():
+    assert isinstance(kgs.ExecutorConfig("serial").build(), kgs.SerialExecutor)
+    assert kgs.ExecutorConfig("phased", 4).build().workers == 4
+    ex = kgs.ExecutorConfig("cuda", 2).build()
+    assert isinstance(ex, kgs.CudaExecutor) and ex.devices == (0, 1)
+    with pytest.raises(ValueError):
+        kgs.ExecutorConfig("gpu", 1)        # reference tests/test_executor.py:23-27
+    with pytest.raises(ValueError):
+        kgs.ExecutorConfig("serial", 0)
+    v = kgs.CudaExecutor((0,), slabs_per_device=4)
+    assert v.nslabs == 4 and v.slab_devices() == (0, 0, 0, 0)
+
+
+def test_integrate_argument_validation():
+    g = kgs.GridSpec(2, 0.0, 1.0, 4)
+    s = kgs.FieldState.zeros(g)
+    sch = kgs.checkerboard_schedule(g)
+    with pytest.raises(ValueError, match="tau > 0"):
+        kgs.integrate(s, g, kgs.PhysParams(), sch, None, 0.0, 1.0)
+    with pytest.raises(ValueError, match="tau > 0"):
+        kgs.integrate(s, g, kgs.PhysParams(), sch, None, 0.1, -1.0)
+    with pytest.raises(ValueError, match="record_stride"):
+        kgs.integrate(s, g, kgs.PhysParams(), sch, None, 0.1, 1.0, record_stride=0)
+
+
+def test_slab_partition_and_rank_sum():
+    cover = []
+    for r in range(4):
+        x0, nx = slab_range(16, r, 4)
+        cover.extend(range(x0, x0 + nx))
+    assert cover == list(range(16))
+    with pytest.raises(ValueError):
+        slab_range(10, 0, 4)
+    t = combine_rank_terms([np.full(8, 1.0), np.full(8, 2.0)])
+    assert np.array_equal(t, np.full(8, 3.0))
+
+
+def test_energy_from_terms_formula():
+    from paper_2502_09537_b200.grid import energy_from_terms
+    g = kgs.GridSpec(2, 0.0, 2.0, 4)        # h = 0.5
+    p = kgs.PhysParams(2.0, 3.0, 0.5, 0.25)
+    t = [1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0]
+    e, m = energy_from_terms(t, p, g)
+    quad = 2.0 * 4.0 + 2.0 * 8.0 + 3.0 * 12.0 + 4.0 + 0.25 * 5.0
+    assert e == pytest.approx(0.25 * (0.5 * quad - 0.25 * 6.0))
+    assert m == pytest.approx(0.25 * 15.0)
