@@ -157,6 +157,20 @@ int64_t kgs_launch_count(kgs_ctx* ctx);
  * measured with CUDA events on the context's stream(s) (max over slabs). */
 double kgs_last_step_ms(kgs_ctx* ctx);
 
+/* Tile/grid tuning of the colour passes (defaults 4, 64, 0, 0): rows per
+ * 256-thread tile of the simple kernel (power of two), band height in rows
+ * for its band-major tile order (<= 0: plane-major), a cap on resident
+ * blocks per SM (0: occupancy maximum), and planes per work unit of the 3-D
+ * marching kernel (0: automatic, < 0: never use the marching kernel).
+ * Results do not depend on these (bitwise). */
+int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
+                   int march_planes);
+
+/* Device self-test: the shared-reciprocal division used by the kernels
+ * against the IEEE `/` on n pseudo-random operand pairs; *mismatches
+ * counts bitwise differences (expected 0). */
+int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatches);
+
 /* Per-launch timing of the fused colour passes (K3 black base+adjoint and
  * K4 red adjoint+base) inside kgs_step_dpavf2: when enabled, a CUDA event
  * pair brackets each such launch on its stream.  kgs_pass_stats returns the
@@ -171,6 +185,11 @@ int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
  * a host round trip; used for >= 512^3 benchmark inputs.  Values agree with
  * the numpy presets to libm rounding, not bitwise. */
 int kgs_fill_preset(kgs_ctx* ctx, int preset);
+
+/* Page-locked host memory for fast asynchronous host<->device copies of
+ * FieldState arrays (cudaHostAlloc / cudaFreeHost). */
+int kgs_host_alloc(int64_t bytes, void** out);
+int kgs_host_free(void* p);
 
 /* ABI version (major*100 + minor). */
 int kgs_abi_version(void);

@@ -100,6 +100,9 @@ struct kgs_ctx {
   double last_ms = 0.0;
   int nsm = 148;
   int grid_cap = 0;  // max persistent grid (blocks), sizes partials
+  // tuning knobs (kgs_set_tuning): rows per tile, band height, blocks/SM cap
+  int tune_ty = 4, tune_band_rows = 64, tune_occ = 0;
+  int tune_xc = 0;  // march kernel planes per unit (0 auto, < 0 disables it)
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
   std::vector<cudaEvent_t> pass_ev;
@@ -159,15 +162,24 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   g.xb = xb;
   g.x0 = s.x0;
   g.wrap = (ctx->slabs.size() == 1 && !(ctx->dist && ctx->nranks > 1)) ? 1 : 0;
-  // 3-D: 64 slots x 4 rows (rows y+-1 reused from L1 inside the tile);
+  // 3-D: tk slots x ty rows (rows y+-1 shared through L1 inside the tile);
   // otherwise one row segment of up to 256 slots.
   int tk = std::min(kThreads, pow2ceil(ctx->nk));
-  if (ctx->d == 3) tk = std::min(tk, 64);
+  if (ctx->d == 3) tk = std::min(tk, kThreads / std::max(1, ctx->tune_ty));
   int ty = std::min(kThreads / tk, pow2ceil(ctx->ny));
   g.tk = tk;
   g.ty = ty;
   g.nkt = (ctx->nk + tk - 1) / tk;
   g.nyt = (ctx->ny + ty - 1) / ty;
+  // y-bands: tiles are visited band by band, and inside a band plane by
+  // plane, so the other colour's planes x-1, x, x+1 of a band are re-read
+  // from L2 a few hundred tiles apart instead of a whole plane apart.
+  int target = std::max(1, ctx->tune_band_rows / ty);
+  int nbt = 1;
+  for (int v = 1; v <= std::min(target, g.nyt); ++v)
+    if (g.nyt % v == 0) nbt = v;
+  if (ctx->tune_band_rows <= 0) nbt = g.nyt;  // no banding
+  g.nbt = nbt;
   g.ntiles = (int64_t)(xb - xa) * g.nyt * g.nkt;
   return g;
 }
@@ -182,7 +194,8 @@ int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
     if (occ < 1) occ = 1;
   }
-  int64_t grid = std::min<int64_t>(g.ntiles, (int64_t)occ * ctx->nsm);
+  const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
+  int64_t grid = std::min<int64_t>(g.ntiles, (int64_t)bps * ctx->nsm);
   grid = std::min<int64_t>(grid, ctx->grid_cap);
   if (grid < 1) return KGS_OK;  // nothing to do
   kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(g, c, s.partials[COL], s.bad,
@@ -193,12 +206,53 @@ int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
   return KGS_OK;
 }
 
+// 3-D march kernel tile (rows x slots); used when it divides the plane.
+constexpr int kMarchTY = 4, kMarchTK = 64;
+
+template <int COL, int OP1, int OP2, bool DIAG, bool CHECK>
+int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
+                 int step_no) {
+  using L = MarchSmem<kMarchTY, kMarchTK>;
+  auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, kMarchTY, kMarchTK>;
+  static int occ = 0;
+  if (occ == 0) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMarchTY * kMarchTK, L::bytes));
+    if (occ < 1) return fail(ctx, KGS_ECUDA, "march kernel does not fit on an SM");
+  }
+  const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
+  const int64_t G = std::min<int64_t>((int64_t)bps * ctx->nsm, ctx->grid_cap);
+  const int64_t cols = (int64_t)(g.ny / kMarchTY) * (g.nk / kMarchTK);
+  const int nxr = g.xb - g.xa;
+  MarchCfg mc;
+  if (ctx->tune_xc > 0) mc.xc = std::min(ctx->tune_xc, nxr);
+  else  // ~8 units per resident block for load balance, >= 8 planes per unit
+    mc.xc = (int)std::max<int64_t>(std::min<int64_t>(nxr, 8), std::min<int64_t>(nxr, (int64_t)nxr * cols / (8 * G)));
+  mc.nunits = (int64_t)((nxr + mc.xc - 1) / mc.xc) * cols;
+  const int64_t grid = std::min<int64_t>(mc.nunits, G);
+  if (grid < 1) return KGS_OK;
+  kern<<<(unsigned)grid, kMarchTY * kMarchTK, L::bytes, s.stream>>>(g, c, s.partials[COL],
+                                                                   s.bad, step_no, mc);
+  ctx->launches++;
+  if (DIAG) s.npart[COL] = (int)grid;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+bool use_march(const kgs_ctx* ctx, const PassGeom& g) {
+  return ctx->d == 3 && ctx->tune_xc >= 0 && g.ny % kMarchTY == 0 && g.nk % kMarchTK == 0 &&
+         g.xb - g.xa >= 1;
+}
+
 template <int D, int COL>
 int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
                int op1, int op2, bool diag, bool check, int step_no) {
-#define KGS_CASE(O1, O2, DG, CH)                                        \
-  if (op1 == O1 && op2 == O2 && diag == DG && check == CH)             \
-    return launch_t<D, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);
+#define KGS_CASE(O1, O2, DG, CH)                                          \
+  if (op1 == O1 && op2 == O2 && diag == DG && check == CH) {             \
+    if (D == 3 && use_march(ctx, g))                                     \
+      return launch_march<COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);   \
+    return launch_t<D, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);      \
+  }
   // single sweeps (kgs_sweep, head)
   KGS_CASE(OP_BASE, OP_NONE, false, false)
   KGS_CASE(OP_ADJ, OP_NONE, false, false)
@@ -786,6 +840,49 @@ int kgs_all_finite(kgs_ctx* ctx, int* ok) {
   r = read_bad(ctx, &bad);
   if (r) return r;
   *ok = (bad == ULLONG_MAX) ? 1 : 0;
+  return KGS_OK;
+}
+
+int kgs_host_alloc(int64_t bytes, void** out) {
+  kgs_ctx* ctx = nullptr;
+  if (!out || bytes < 0) return fail(nullptr, KGS_EINVAL, "bad arguments");
+  *out = nullptr;
+  CK(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 8), cudaHostAllocPortable));
+  return KGS_OK;
+}
+
+int kgs_host_free(void* p) {
+  kgs_ctx* ctx = nullptr;
+  if (p) CK(cudaFreeHost(p));
+  return KGS_OK;
+}
+
+int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
+                   int march_planes) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  if (rows_per_tile < 1 || rows_per_tile > kThreads || (rows_per_tile & (rows_per_tile - 1)))
+    return fail(ctx, KGS_EINVAL, "rows_per_tile must be a power of two in [1, 256]");
+  ctx->tune_ty = rows_per_tile;
+  ctx->tune_band_rows = band_rows;
+  ctx->tune_occ = blocks_per_sm;
+  ctx->tune_xc = march_planes;
+  return KGS_OK;
+}
+
+int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatches) {
+  kgs_ctx* ctx = nullptr;
+  if (!mismatches || n < 0) return fail(nullptr, KGS_EINVAL, "bad arguments");
+  CK(cudaSetDevice(device));
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, sizeof *d));
+  CK(cudaMemset(d, 0, sizeof *d));
+  division_selftest<<<1184, 256>>>(n, (unsigned long long)seed, d);
+  cudaError_t e = cudaGetLastError();
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(nullptr, KGS_ECUDA, "division self-test: %s", cudaGetErrorString(e));
+  *mismatches = (int64_t)h;
   return KGS_OK;
 }
 

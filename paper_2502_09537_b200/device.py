@@ -189,6 +189,11 @@ class DeviceContext:
     def last_step_ms(self) -> float:
         return float(_lib.load().kgs_last_step_ms(self.ptr))
 
+    def set_tuning(self, rows_per_tile: int = 4, band_rows: int = 64,
+                   blocks_per_sm: int = 0, march_planes: int = 0) -> None:
+        self.check(_lib.load().kgs_set_tuning(self.ptr, rows_per_tile, band_rows,
+                                              blocks_per_sm, march_planes))
+
     def pass_timing(self, enable: bool) -> None:
         self.check(_lib.load().kgs_pass_timing(self.ptr, int(enable)))
 
@@ -288,10 +293,25 @@ def as_device_state(state, grid: GridSpec, executor=None):
     return DeviceFieldState(grid, context=ctx, t=state.t), True
 
 
+class _PinnedBlock:
+    """Owner of one cudaHostAlloc block; freed when the last array view dies."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _lib.check(_lib.load().kgs_host_alloc(nbytes, ctypes.byref(p)))
+        self.ptr = p
+
+    def __del__(self):
+        try:
+            if self.ptr.value:
+                _lib.load().kgs_host_free(self.ptr)
+        except Exception:
+            pass
+
+
 def pinned_empty(n: int) -> np.ndarray:
-    """float64[n] in page-locked host memory (via torch's pinned allocator)."""
-    import torch
-    t = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    a = t.numpy()
-    a.flags.writeable = True
-    return a
+    """float64[n] in page-locked host memory (cudaHostAlloc via the C ABI)."""
+    block = _PinnedBlock(8 * n)
+    buf = (ctypes.c_double * n).from_address(block.ptr.value)
+    buf._owner = block          # keep the block alive as long as the buffer
+    return np.ctypeslib.as_array(buf)

@@ -212,3 +212,31 @@ def test_1024cubed_full_size_smoke():
     assert dev.is_finite()
     assert tr.max_rel_error() < 1e-11
     dev.close()
+
+
+def test_shared_reciprocal_division():
+    """The kernels' shared-reciprocal quotient is bit-identical to IEEE `/`."""
+    import ctypes
+    from paper_2502_09537_b200 import _lib
+    bad = ctypes.c_int64(-1)
+    _lib.check(_lib.load().kgs_selftest_division(0, 1 << 26, 12345, ctypes.byref(bad)))
+    assert bad.value == 0
+
+
+@pytest.mark.parametrize("xc", [0, 3, 8, 128])
+def test_march_kernel_matches_simple_kernel(xc):
+    """3-D marching (cp.async ring) kernel == simple per-point kernel, bitwise,
+    for several work-unit sizes (incl. a non-divisor of the slab)."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    outs = []
+    for planes in (-1, xc):
+        dev = kgs.DeviceFieldState.from_host(s0, g)
+        dev.ctx.set_tuning(march_planes=planes)
+        terms, _ = dev.ctx.step_dpavf2(args, 5, 0, 5)
+        outs.append((dev.to_host(), terms))
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-13)
