@@ -157,14 +157,21 @@ int64_t kgs_launch_count(kgs_ctx* ctx);
  * measured with CUDA events on the context's stream(s) (max over slabs). */
 double kgs_last_step_ms(kgs_ctx* ctx);
 
-/* Tile/grid tuning of the colour passes (defaults 4, 64, 0, 0): rows per
- * 256-thread tile of the simple kernel (power of two), band height in rows
- * for its band-major tile order (<= 0: plane-major), a cap on resident
- * blocks per SM (0: occupancy maximum), and planes per work unit of the 3-D
- * marching kernel (0: automatic, < 0: never use the marching kernel).
- * Results do not depend on these (bitwise). */
+/* Tile/grid tuning of the colour passes (defaults 4, 64, 0, 0, 1): rows
+ * per 256-thread tile of the simple kernel (power of two), band height in
+ * rows for its band-major tile order (<= 0: plane-major), a cap on resident
+ * blocks per SM (0: occupancy maximum), planes per work unit of the 3-D
+ * marching kernel (0: automatic, < 0: never use the marching kernel), and
+ * the marching kernel's tile variant (0: 4x64, 1: 8x64, 2: 16x32, 3: 32x32
+ * rows x slots; < 0: keep).  Results do not depend on these (bitwise). */
 int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
-                   int march_planes);
+                   int march_planes, int march_variant);
+
+/* Benchmarking only (CORRUPTS the resident state): average device time of
+ * `reps` black fused passes of the marching kernel in a debug mode:
+ * 0 = normal, 1 = no arithmetic (data movement only), 2 = no ghost-cell
+ * stores, 3 = no stores.  Used to measure the pass's memory ceiling. */
+int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out);
 
 /* Device self-test: the shared-reciprocal division used by the kernels
  * against the IEEE `/` on n pseudo-random operand pairs; *mismatches

@@ -31,7 +31,7 @@ EXPORTED = (
     "kgs_all_finite", "kgs_last_error", "kgs_launch_count",
     "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version",
     "kgs_pass_timing", "kgs_pass_stats", "kgs_host_alloc", "kgs_host_free",
-    "kgs_set_tuning", "kgs_selftest_division",
+    "kgs_set_tuning", "kgs_selftest_division", "kgs_debug_pass",
 )
 
 
@@ -98,9 +98,10 @@ def load() -> ctypes.CDLL:
         "kgs_host_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(_P)]),
         "kgs_host_free": (ctypes.c_int, [_P]),
         "kgs_set_tuning": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                          ctypes.c_int]),
+                                          ctypes.c_int, ctypes.c_int]),
         "kgs_selftest_division": (ctypes.c_int, [ctypes.c_int, _I64, ctypes.c_uint64,
                                                  ctypes.POINTER(_I64)]),
+        "kgs_debug_pass": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -70,7 +70,10 @@ struct Slab {
   int64_t x0 = 0;  // global first plane
   int nx = 0;      // planes
   double* buf[2] = {nullptr, nullptr};    // colour c, ghost plane -1
-  double* plane0[2] = {nullptr, nullptr}; // colour c, plane 0
+  double* plane0[2] = {nullptr, nullptr}; // colour c, element (x=0,f=0,y=0,k=0)
+  CUtensorMap tm_halo[4][2];  // [march variant][colour]: other-colour tile + halo box
+  CUtensorMap tm_tile[4][2];  // [march variant][colour]: own tile box
+  bool has_tmaps[4] = {false, false, false, false};  // variant fits this geometry
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
   double* records = nullptr;                 // device [cap * NTERMS]
@@ -90,7 +93,10 @@ struct kgs_ctx {
   double a = 0, b = 1, h = 1;
   int ny = 1, nk = 1, nz = 1;   // rows per plane, slots per row, natural row
   int64_t nxg = 1;              // global planes
-  int64_t pp = 0, ps = 0;       // points per plane & colour, plane stride
+  int rs = 0;                   // row stride (nk + 2*GK)
+  int gy = 0;                   // ghost rows per side (1 for d == 3)
+  int64_t org = 0;              // offset of (y=0, k=0) in a field-plane
+  int64_t pp = 0, ps = 0;       // field stride in a plane, plane stride
   std::vector<Slab> slabs;
   bool dist = false;
   int rank = 0, nranks = 1;
@@ -103,6 +109,7 @@ struct kgs_ctx {
   // tuning knobs (kgs_set_tuning): rows per tile, band height, blocks/SM cap
   int tune_ty = 4, tune_band_rows = 64, tune_occ = 0;
   int tune_xc = 0;  // march kernel planes per unit (0 auto, < 0 disables it)
+  int tune_variant = 1;  // march kernel tile variant (MV0..MV3)
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
   std::vector<cudaEvent_t> pass_ev;
@@ -155,6 +162,8 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   g.oth = s.plane0[col ^ 1];
   g.ps = ctx->ps;
   g.pp = ctx->pp;
+  g.rs = ctx->rs;
+  g.ghosts = ctx->d == 3 ? 1 : 0;
   g.nx = s.nx;
   g.ny = ctx->ny;
   g.nk = ctx->nk;
@@ -206,42 +215,126 @@ int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
   return KGS_OK;
 }
 
-// 3-D march kernel tile (rows x slots); used when it divides the plane.
-constexpr int kMarchTY = 4, kMarchTK = 64;
+// ---- TMA descriptors ------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <int COL, int OP1, int OP2, bool DIAG, bool CHECK>
-int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
-                 int step_no) {
-  using L = MarchSmem<kMarchTY, kMarchTK>;
-  auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, kMarchTY, kMarchTK>;
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 3-D march kernel variants: tile rows x slots, ring depths, min blocks/SM.
+// Larger tile cross-sections re-read fewer halo rows/slots.
+template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_>
+struct MarchVariant {
+  static constexpr int TY = TY_, TK = TK_, NOTH = NOTH_, NOWN = NOWN_, MINB = MINB_;
+  static constexpr int NT = TY * TK;
+  using L = MarchSmem<TY, TK, NOTH, NOWN>;
+};
+using MV0 = MarchVariant<4, 64, 4, 2, 4>;     // 256 threads, 4 blocks/SM
+using MV1 = MarchVariant<8, 64, 4, 2, 2>;     // 512 threads, 2 blocks/SM
+using MV2 = MarchVariant<16, 32, 4, 2, 2>;    // 512 threads, 2 blocks/SM
+using MV3 = MarchVariant<32, 32, 4, 2, 1>;    // 1024 threads, 1 block/SM
+constexpr int kMarchVariants = 4;
+constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY};
+constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK};
+constexpr int kVarRS[kMarchVariants] = {MV0::L::RS, MV1::L::RS, MV2::L::RS, MV3::L::RS};
+constexpr int kVarRO[kMarchVariants] = {MV0::L::RO, MV1::L::RO, MV2::L::RO, MV3::L::RO};
+
+// 4-D view of one colour array: (slot incl. ghosts, row incl. ghosts, field,
+// plane incl. ghosts); per variant two box shapes: the other-colour tile +
+// halo (P, Q, U) and the own tile (P, Q, U, V).
+int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)ctx->rs, (cuuint64_t)(ctx->ny + 2 * ctx->gy), 4,
+                              (cuuint64_t)(s.nx + 2)};
+  const cuuint64_t strides[3] = {(cuuint64_t)ctx->rs * 8, (cuuint64_t)ctx->pp * 8,
+                                 (cuuint64_t)ctx->ps * 8};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  for (int v = 0; v < kMarchVariants; ++v) {
+    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % kVarTY[v] == 0 && ctx->nk % kVarTK[v] == 0 &&
+                     (ctx->rs * 8) % 16 == 0;
+    if (!s.has_tmaps[v]) continue;
+    const cuuint32_t halo_box[4] = {(cuuint32_t)kVarRS[v], (cuuint32_t)kVarRO[v], 3, 1};
+    const cuuint32_t tile_box[4] = {(cuuint32_t)kVarTK[v], (cuuint32_t)kVarTY[v], 4, 1};
+    for (int c = 0; c < 2; ++c) {
+      CUresult r1 = enc(&s.tm_halo[v][c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf[c], dims,
+                        strides, halo_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CUresult r2 = enc(&s.tm_tile[v][c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf[c], dims,
+                        strides, tile_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+        return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled failed (%d, %d)", (int)r1, (int)r2);
+    }
+  }
+  return KGS_OK;
+}
+
+template <typename Var, int COL, int OP1, int OP2, bool DIAG, bool CHECK, int DBG = 0>
+int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
+                 int v) {
+  using L = typename Var::L;
+  auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
+                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG>;
   static int occ = 0;
   if (occ == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMarchTY * kMarchTK, L::bytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Var::NT, L::bytes));
     if (occ < 1) return fail(ctx, KGS_ECUDA, "march kernel does not fit on an SM");
   }
   const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
   const int64_t G = std::min<int64_t>((int64_t)bps * ctx->nsm, ctx->grid_cap);
-  const int64_t cols = (int64_t)(g.ny / kMarchTY) * (g.nk / kMarchTK);
+  const int64_t cols = (int64_t)(g.ny / Var::TY) * (g.nk / Var::TK);
   const int nxr = g.xb - g.xa;
   MarchCfg mc;
   if (ctx->tune_xc > 0) mc.xc = std::min(ctx->tune_xc, nxr);
   else  // ~8 units per resident block for load balance, >= 8 planes per unit
-    mc.xc = (int)std::max<int64_t>(std::min<int64_t>(nxr, 8), std::min<int64_t>(nxr, (int64_t)nxr * cols / (8 * G)));
+    mc.xc = (int)std::max<int64_t>(std::min<int64_t>(nxr, 8),
+                                   std::min<int64_t>(nxr, (int64_t)nxr * cols / (8 * G)));
   mc.nunits = (int64_t)((nxr + mc.xc - 1) / mc.xc) * cols;
   const int64_t grid = std::min<int64_t>(mc.nunits, G);
   if (grid < 1) return KGS_OK;
-  kern<<<(unsigned)grid, kMarchTY * kMarchTK, L::bytes, s.stream>>>(g, c, s.partials[COL],
-                                                                   s.bad, step_no, mc);
+  kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
+      s.tm_halo[v][COL ^ 1], s.tm_tile[v][COL], g, c, s.partials[COL], s.bad, step_no, mc);
   ctx->launches++;
   if (DIAG) s.npart[COL] = (int)grid;
   CK(cudaGetLastError());
   return KGS_OK;
 }
 
-bool use_march(const kgs_ctx* ctx, const PassGeom& g) {
-  return ctx->d == 3 && ctx->tune_xc >= 0 && g.ny % kMarchTY == 0 && g.nk % kMarchTK == 0 &&
-         g.xb - g.xa >= 1;
+// march variant to use for this pass, or -1 for the simple kernel
+int march_variant(const kgs_ctx* ctx, const Slab& s, const PassGeom& g) {
+  if (ctx->d != 3 || ctx->tune_xc < 0 || g.xb - g.xa < 1) return -1;
+  int v = ctx->tune_variant;
+  if (v >= 0 && v < kMarchVariants && s.has_tmaps[v]) return v;
+  for (v = 0; v < kMarchVariants; ++v)   // fall back to any eligible variant
+    if (s.has_tmaps[v]) return v;
+  return -1;
+}
+
+template <int COL, int O1, int O2, bool DG, bool CH>
+int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
+                     int v) {
+  switch (v) {
+    case 0: return launch_march<MV0, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 1: return launch_march<MV1, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 2: return launch_march<MV2, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    default: return launch_march<MV3, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+  }
 }
 
 template <int D, int COL>
@@ -249,8 +342,11 @@ int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
                int op1, int op2, bool diag, bool check, int step_no) {
 #define KGS_CASE(O1, O2, DG, CH)                                          \
   if (op1 == O1 && op2 == O2 && diag == DG && check == CH) {             \
-    if (D == 3 && use_march(ctx, g))                                     \
-      return launch_march<COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);   \
+    if (D == 3) {                                                        \
+      const int v_ = march_variant(ctx, s, g);                           \
+      if (v_ >= 0)                                                       \
+        return launch_march_any<COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v_); \
+    }                                                                    \
     return launch_t<D, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);      \
   }
   // single sweeps (kgs_sweep, head)
@@ -297,7 +393,7 @@ int exchange(kgs_ctx* ctx, int col) {
     Slab& s = ctx->slabs[0];
     const int up = (ctx->rank + 1) % ctx->nranks;
     const int dn = (ctx->rank - 1 + ctx->nranks) % ctx->nranks;
-    double* p0 = s.plane0[col];
+    double* p0 = s.plane0[col] - ctx->org;  // plane 0 start (ghost rows/slots included)
     NK(g_nccl.GroupStart());
     // order matters when up == dn (2 ranks): sends [to dn: plane 0, to up:
     // plane nx-1]; recvs [from up: ghost nx, from dn: ghost -1].
@@ -324,10 +420,10 @@ int exchange(kgs_ctx* ctx, int col) {
     CK(cudaStreamWaitEvent(s.stream, lo.ev_done, 0));
     CK(cudaStreamWaitEvent(s.stream, hi.ev_done, 0));
     // pull: ghost -1 <- lo plane nx-1 ; ghost nx <- hi plane 0
-    double* g_lo = s.plane0[col] - ctx->ps;
-    double* g_hi = s.plane0[col] + (int64_t)s.nx * ctx->ps;
-    const double* src_lo = lo.plane0[col] + (int64_t)(lo.nx - 1) * ctx->ps;
-    const double* src_hi = hi.plane0[col];
+    double* g_lo = s.plane0[col] - ctx->org - ctx->ps;
+    double* g_hi = s.plane0[col] - ctx->org + (int64_t)s.nx * ctx->ps;
+    const double* src_lo = lo.plane0[col] - ctx->org + (int64_t)(lo.nx - 1) * ctx->ps;
+    const double* src_hi = hi.plane0[col] - ctx->org;
     if (lo.dev == s.dev)
       CK(cudaMemcpyAsync(g_lo, src_lo, face * 8, cudaMemcpyDeviceToDevice, s.stream));
     else
@@ -449,6 +545,7 @@ Coeffs to_coeffs(const kgs_coeffs* c) {
   return k;
 }
 
+
 int alloc_slab(kgs_ctx* ctx, Slab& s) {
   CK(cudaSetDevice(s.dev));
   const size_t colour_bytes = (size_t)(s.nx + 2) * ctx->ps * sizeof(double);
@@ -460,8 +557,12 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
                   colour_bytes, cudaGetErrorString(e));
     }
     CK(cudaMemset(s.buf[c], 0, colour_bytes));
-    s.plane0[c] = s.buf[c] + ctx->ps;
+    s.plane0[c] = s.buf[c] + ctx->ps + ctx->org;
     CK(cudaMalloc(&s.partials[c], (size_t)ctx->grid_cap * NTERMS * sizeof(double)));
+  }
+  if (ctx->d == 3) {
+    int r = make_tensor_maps(ctx, s);
+    if (r) return r;
   }
   CK(cudaMalloc(&s.bad, sizeof(unsigned long long)));
   CK(cudaMemset(s.bad, 0xff, sizeof(unsigned long long)));
@@ -494,7 +595,10 @@ int init_geometry(kgs_ctx* ctx, int d, int64_t N, double a, double b) {
   ctx->nk = (int)(N / 2);
   ctx->ny = (d == 3) ? (int)N : 1;
   ctx->nxg = (d >= 2) ? N : 1;
-  ctx->pp = (int64_t)ctx->ny * ctx->nk;
+  ctx->rs = ctx->nk + 2 * GK;
+  ctx->gy = (d == 3) ? 1 : 0;
+  ctx->org = (int64_t)ctx->gy * ctx->rs + GK;
+  ctx->pp = (int64_t)(ctx->ny + 2 * ctx->gy) * ctx->rs;
   ctx->ps = 4 * ctx->pp;
   return KGS_OK;
 }
@@ -668,11 +772,13 @@ int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
         const double* src = f[fi] + (s.x0 - base_x + xs) * nat_plane;
         CK(cudaMemcpyAsync(s.stage, src, (size_t)nxc * nat_plane * 8,
                            cudaMemcpyHostToDevice, s.stream));
-        const int64_t n = (int64_t)nxc * ctx->pp;
+        const int64_t n = (int64_t)nxc * ctx->ny * ctx->nk;
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
-        split_field<<<blocks, 256, 0, s.stream>>>(
-            s.stage, s.plane0[1] + fi * ctx->pp, s.plane0[0] + fi * ctx->pp,
-            ctx->ps, ctx->pp, nxc, ctx->ny, ctx->nk, xs, s.x0);
+        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
+        g.own += fi * ctx->pp;
+        g.oth += fi * ctx->pp;
+        split_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs,
+                                                  (ctx->d == 3 && fi < 3) ? 1 : 0);
         ctx->launches++;
         CK(cudaGetLastError());
       }
@@ -694,11 +800,12 @@ int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V) {
     for (int fi = 0; fi < 4; ++fi) {
       for (int xs = 0; xs < s.nx; xs += s.stage_planes) {
         const int nxc = std::min(s.stage_planes, s.nx - xs);
-        const int64_t n = (int64_t)nxc * ctx->pp;
+        const int64_t n = (int64_t)nxc * ctx->ny * ctx->nk;
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
-        merge_field<<<blocks, 256, 0, s.stream>>>(
-            s.stage, s.plane0[1] + fi * ctx->pp, s.plane0[0] + fi * ctx->pp,
-            ctx->ps, ctx->pp, nxc, ctx->ny, ctx->nk, xs, s.x0);
+        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
+        g.own += fi * ctx->pp;
+        g.oth += fi * ctx->pp;
+        merge_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs);
         ctx->launches++;
         CK(cudaGetLastError());
         double* dst = f[fi] + (s.x0 - base_x + xs) * nat_plane;
@@ -858,7 +965,7 @@ int kgs_host_free(void* p) {
 }
 
 int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
-                   int march_planes) {
+                   int march_planes, int march_variant) {
   if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
   if (rows_per_tile < 1 || rows_per_tile > kThreads || (rows_per_tile & (rows_per_tile - 1)))
     return fail(ctx, KGS_EINVAL, "rows_per_tile must be a power of two in [1, 256]");
@@ -866,7 +973,46 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
   ctx->tune_band_rows = band_rows;
   ctx->tune_occ = blocks_per_sm;
   ctx->tune_xc = march_planes;
+  if (march_variant >= 0) ctx->tune_variant = march_variant;
   return KGS_OK;
+}
+
+int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
+  if (!ctx || !ms_out || reps < 1) return fail(ctx, KGS_EINVAL, "bad arguments");
+  Slab& s = ctx->slabs[0];
+  PassGeom g = make_geom(ctx, s, 0, 0, s.nx);
+  const int v = march_variant(ctx, s, g);
+  if (v != 0 && v != 1) return fail(ctx, KGS_EINVAL, "debug pass needs march variant 0 or 1");
+  Coeffs c{};
+  CK(cudaSetDevice(s.dev));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  int r = KGS_OK;
+  for (int i = 0; i <= reps && !r; ++i) {
+    if (i == 1) CK(cudaEventRecord(a, s.stream));
+#define KGS_DBG(M)                                                                       \
+  r = (v == 0) ? launch_march<MV0, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v) \
+               : launch_march<MV1, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v);
+    switch (mode) {
+      case 0: KGS_DBG(0) break;
+      case 1: KGS_DBG(1) break;
+      case 2: KGS_DBG(2) break;
+      case 3: KGS_DBG(3) break;
+      case 4: KGS_DBG(4) break;
+      case 5: KGS_DBG(5) break;
+      default: KGS_DBG(6) break;
+    }
+#undef KGS_DBG
+  }
+  CK(cudaEventRecord(b, s.stream));
+  CK(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms_out = ms / reps;
+  return r;
 }
 
 int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatches) {
@@ -901,7 +1047,7 @@ int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
   if (launches) *launches = ctx->pass_count;
   if (total_ms) *total_ms = ctx->pass_ms;
   int64_t pts = 0;
-  for (auto& s : ctx->slabs) pts += (int64_t)s.nx * ctx->pp;  // one colour
+  for (auto& s : ctx->slabs) pts += (int64_t)s.nx * ctx->ny * ctx->nk;  // one colour
   if (points_per_launch) *points_per_launch = pts;
   return KGS_OK;
 }
@@ -915,11 +1061,10 @@ int kgs_fill_preset(kgs_ctx* ctx, int preset) {
                 need_d[preset], ctx->d);
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
-    const int64_t n = (int64_t)s.nx * ctx->pp * 2;
+    const int64_t n = (int64_t)s.nx * ctx->ny * ctx->nk * 2;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
-    fill_preset<<<blocks, 256, 0, s.stream>>>(s.plane0[0], s.plane0[1], ctx->ps,
-                                              ctx->pp, s.nx, ctx->ny, ctx->nk, s.x0,
-                                              ctx->d, ctx->a, ctx->h, preset);
+    PassGeom g = make_geom(ctx, s, 0, 0, s.nx);   // own = black, oth = red
+    fill_preset<<<blocks, 256, 0, s.stream>>>(g, ctx->a, ctx->h, preset, ctx->d == 3 ? 1 : 0);
     ctx->launches++;
     CK(cudaGetLastError());
   }

@@ -190,9 +190,10 @@ class DeviceContext:
         return float(_lib.load().kgs_last_step_ms(self.ptr))
 
     def set_tuning(self, rows_per_tile: int = 4, band_rows: int = 64,
-                   blocks_per_sm: int = 0, march_planes: int = 0) -> None:
+                   blocks_per_sm: int = 0, march_planes: int = 0,
+                   march_variant: int = -1) -> None:
         self.check(_lib.load().kgs_set_tuning(self.ptr, rows_per_tile, band_rows,
-                                              blocks_per_sm, march_planes))
+                                              blocks_per_sm, march_planes, march_variant))
 
     def pass_timing(self, enable: bool) -> None:
         self.check(_lib.load().kgs_pass_timing(self.ptr, int(enable)))

@@ -223,10 +223,10 @@ def test_shared_reciprocal_division():
     assert bad.value == 0
 
 
-@pytest.mark.parametrize("xc", [0, 3, 8, 128])
-def test_march_kernel_matches_simple_kernel(xc):
-    """3-D marching (cp.async ring) kernel == simple per-point kernel, bitwise,
-    for several work-unit sizes (incl. a non-divisor of the slab)."""
+@pytest.mark.parametrize("variant,xc", [(1, 0), (1, 3), (1, 128), (0, 8), (2, 5), (3, 0)])
+def test_march_kernel_matches_simple_kernel(variant, xc):
+    """3-D marching (TMA ring) kernel == simple per-point kernel, bitwise, for
+    every tile variant and several work-unit sizes (incl. a non-divisor)."""
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(128)
     s0 = sc.state(g)
@@ -234,7 +234,7 @@ def test_march_kernel_matches_simple_kernel(xc):
     outs = []
     for planes in (-1, xc):
         dev = kgs.DeviceFieldState.from_host(s0, g)
-        dev.ctx.set_tuning(march_planes=planes)
+        dev.ctx.set_tuning(march_planes=planes, march_variant=variant)
         terms, _ = dev.ctx.step_dpavf2(args, 5, 0, 5)
         outs.append((dev.to_host(), terms))
         dev.close()
