@@ -157,7 +157,7 @@ int64_t kgs_launch_count(kgs_ctx* ctx);
  * measured with CUDA events on the context's stream(s) (max over slabs). */
 double kgs_last_step_ms(kgs_ctx* ctx);
 
-/* Tile/grid tuning of the colour passes (defaults 4, 64, 0, 0, 1): rows
+/* Tile/grid tuning of the colour passes (defaults 4, 64, 0, 0, 0): rows
  * per 256-thread tile of the simple kernel (power of two), band height in
  * rows for its band-major tile order (<= 0: plane-major), a cap on resident
  * blocks per SM (0: occupancy maximum), planes per work unit of the 3-D
@@ -166,6 +166,11 @@ double kgs_last_step_ms(kgs_ctx* ctx);
  * rows x slots; < 0: keep).  Results do not depend on these (bitwise). */
 int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
                    int march_planes, int march_variant);
+
+/* L2 sector promotion of the marching kernel's TMA boxes (0 none, 1 64 B,
+ * 2 128 B, 3 256 B) for the other-colour halo box and the own tile box;
+ * default 0, 0.  Results do not depend on it. */
+int kgs_set_promotion(kgs_ctx* ctx, int halo, int tile);
 
 /* Benchmarking only (CORRUPTS the resident state): average device time of
  * `reps` black fused passes of the marching kernel in a debug mode:

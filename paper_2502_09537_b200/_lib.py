@@ -32,6 +32,7 @@ EXPORTED = (
     "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version",
     "kgs_pass_timing", "kgs_pass_stats", "kgs_host_alloc", "kgs_host_free",
     "kgs_set_tuning", "kgs_selftest_division", "kgs_debug_pass",
+    "kgs_set_promotion",
 )
 
 
@@ -102,6 +103,7 @@ def load() -> ctypes.CDLL:
         "kgs_selftest_division": (ctypes.c_int, [ctypes.c_int, _I64, ctypes.c_uint64,
                                                  ctypes.POINTER(_I64)]),
         "kgs_debug_pass": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
+        "kgs_set_promotion": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

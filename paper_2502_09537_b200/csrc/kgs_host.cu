@@ -71,8 +71,7 @@ struct Slab {
   int nx = 0;      // planes
   double* buf[2] = {nullptr, nullptr};    // colour c, ghost plane -1
   double* plane0[2] = {nullptr, nullptr}; // colour c, element (x=0,f=0,y=0,k=0)
-  CUtensorMap tm_halo[4][2];  // [march variant][colour]: other-colour tile + halo box
-  CUtensorMap tm_tile[4][2];  // [march variant][colour]: own tile box
+  MarchMaps maps[4][2];  // [march variant][colour]: TMA descriptors
   bool has_tmaps[4] = {false, false, false, false};  // variant fits this geometry
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
@@ -93,10 +92,8 @@ struct kgs_ctx {
   double a = 0, b = 1, h = 1;
   int ny = 1, nk = 1, nz = 1;   // rows per plane, slots per row, natural row
   int64_t nxg = 1;              // global planes
-  int rs = 0;                   // row stride (nk + 2*GK)
-  int gy = 0;                   // ghost rows per side (1 for d == 3)
-  int64_t org = 0;              // offset of (y=0, k=0) in a field-plane
-  int64_t pp = 0, ps = 0;       // field stride in a plane, plane stride
+  int rs = 0;                   // row stride (nk)
+  int64_t pp = 0, ps = 0;       // field stride in a plane (ny*nk), plane stride
   std::vector<Slab> slabs;
   bool dist = false;
   int rank = 0, nranks = 1;
@@ -109,7 +106,8 @@ struct kgs_ctx {
   // tuning knobs (kgs_set_tuning): rows per tile, band height, blocks/SM cap
   int tune_ty = 4, tune_band_rows = 64, tune_occ = 0;
   int tune_xc = 0;  // march kernel planes per unit (0 auto, < 0 disables it)
-  int tune_variant = 1;  // march kernel tile variant (MV0..MV3)
+  int tune_variant = 0;  // march kernel tile variant (MV0..MV3)
+  int tune_promo_halo = 0, tune_promo_tile = 0;  // TMA L2 promotion (0 none .. 3 256B)
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
   std::vector<cudaEvent_t> pass_ev;
@@ -163,7 +161,6 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   g.ps = ctx->ps;
   g.pp = ctx->pp;
   g.rs = ctx->rs;
-  g.ghosts = ctx->d == 3 ? 1 : 0;
   g.nx = s.nx;
   g.ny = ctx->ny;
   g.nk = ctx->nk;
@@ -248,37 +245,52 @@ using MV3 = MarchVariant<32, 32, 4, 2, 1>;    // 1024 threads, 1 block/SM
 constexpr int kMarchVariants = 4;
 constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY};
 constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK};
-constexpr int kVarRS[kMarchVariants] = {MV0::L::RS, MV1::L::RS, MV2::L::RS, MV3::L::RS};
-constexpr int kVarRO[kMarchVariants] = {MV0::L::RO, MV1::L::RO, MV2::L::RO, MV3::L::RO};
 
-// 4-D view of one colour array: (slot incl. ghosts, row incl. ghosts, field,
-// plane incl. ghosts); per variant two box shapes: the other-colour tile +
-// halo (P, Q, U) and the own tile (P, Q, U, V).
+// L2 sector promotion of the TMA boxes.  The two-slot halo columns are 16 B
+// inside a neighbouring tile's lines: promoting them to 256-B fetches would
+// pull whole blocks of that tile from HBM.
+CUtensorMapL2promotion promo(int v) {
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
+// 4-D view of one colour array with dims ordered (slot, field, row, plane)
+// -- strides 8, pp*8, nk*8, ps*8 bytes -- so that a box lands in shared
+// memory as [row][field][slot] (MarchSmem); per variant four box shapes.
 int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[4] = {(cuuint64_t)ctx->rs, (cuuint64_t)(ctx->ny + 2 * ctx->gy), 4,
+  const cuuint64_t dims[4] = {(cuuint64_t)ctx->nk, 4, (cuuint64_t)ctx->ny,
                               (cuuint64_t)(s.nx + 2)};
-  const cuuint64_t strides[3] = {(cuuint64_t)ctx->rs * 8, (cuuint64_t)ctx->pp * 8,
+  const cuuint64_t strides[3] = {(cuuint64_t)ctx->pp * 8, (cuuint64_t)ctx->rs * 8,
                                  (cuuint64_t)ctx->ps * 8};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   for (int v = 0; v < kMarchVariants; ++v) {
-    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % kVarTY[v] == 0 && ctx->nk % kVarTK[v] == 0 &&
-                     (ctx->rs * 8) % 16 == 0;
+    const int ty = kVarTY[v], tk = kVarTK[v];
+    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % ty == 0 && ctx->nk % tk == 0 &&
+                     ctx->nk >= 2 && (ctx->rs * 8) % 16 == 0;
     if (!s.has_tmaps[v]) continue;
-    const cuuint32_t halo_box[4] = {(cuuint32_t)kVarRS[v], (cuuint32_t)kVarRO[v], 3, 1};
-    const cuuint32_t tile_box[4] = {(cuuint32_t)kVarTK[v], (cuuint32_t)kVarTY[v], 4, 1};
+    const cuuint32_t centre[4] = {(cuuint32_t)tk, 3, (cuuint32_t)ty, 1};
+    const cuuint32_t row[4] = {(cuuint32_t)tk, 3, 1, 1};
+    const cuuint32_t col[4] = {2, 3, (cuuint32_t)ty, 1};
+    const cuuint32_t own[4] = {(cuuint32_t)tk, 4, (cuuint32_t)ty, 1};
     for (int c = 0; c < 2; ++c) {
-      CUresult r1 = enc(&s.tm_halo[v][c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf[c], dims,
-                        strides, halo_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      CUresult r2 = enc(&s.tm_tile[v][c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf[c], dims,
-                        strides, tile_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
-        return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled failed (%d, %d)", (int)r1, (int)r2);
+      MarchMaps& m = s.maps[v][c];
+      CUtensorMap* outs[4] = {&m.centre, &m.row, &m.col, &m.own};
+      const cuuint32_t* boxes[4] = {centre, row, col, own};
+      for (int i = 0; i < 4; ++i) {
+        CUresult r = enc(outs[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf[c], dims, strides,
+                         boxes[i], es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         promo(i == 3 ? ctx->tune_promo_tile : ctx->tune_promo_halo),
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+          return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled(variant %d, box %d) failed: %d", v,
+                      i, (int)r);
+      }
     }
   }
   return KGS_OK;
@@ -309,7 +321,7 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   const int64_t grid = std::min<int64_t>(mc.nunits, G);
   if (grid < 1) return KGS_OK;
   kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
-      s.tm_halo[v][COL ^ 1], s.tm_tile[v][COL], g, c, s.partials[COL], s.bad, step_no, mc);
+      s.maps[v][COL ^ 1], s.maps[v][COL], g, c, s.partials[COL], s.bad, step_no, mc);
   ctx->launches++;
   if (DIAG) s.npart[COL] = (int)grid;
   CK(cudaGetLastError());
@@ -393,7 +405,7 @@ int exchange(kgs_ctx* ctx, int col) {
     Slab& s = ctx->slabs[0];
     const int up = (ctx->rank + 1) % ctx->nranks;
     const int dn = (ctx->rank - 1 + ctx->nranks) % ctx->nranks;
-    double* p0 = s.plane0[col] - ctx->org;  // plane 0 start (ghost rows/slots included)
+    double* p0 = s.plane0[col];
     NK(g_nccl.GroupStart());
     // order matters when up == dn (2 ranks): sends [to dn: plane 0, to up:
     // plane nx-1]; recvs [from up: ghost nx, from dn: ghost -1].
@@ -420,10 +432,10 @@ int exchange(kgs_ctx* ctx, int col) {
     CK(cudaStreamWaitEvent(s.stream, lo.ev_done, 0));
     CK(cudaStreamWaitEvent(s.stream, hi.ev_done, 0));
     // pull: ghost -1 <- lo plane nx-1 ; ghost nx <- hi plane 0
-    double* g_lo = s.plane0[col] - ctx->org - ctx->ps;
-    double* g_hi = s.plane0[col] - ctx->org + (int64_t)s.nx * ctx->ps;
-    const double* src_lo = lo.plane0[col] - ctx->org + (int64_t)(lo.nx - 1) * ctx->ps;
-    const double* src_hi = hi.plane0[col] - ctx->org;
+    double* g_lo = s.plane0[col] - ctx->ps;
+    double* g_hi = s.plane0[col] + (int64_t)s.nx * ctx->ps;
+    const double* src_lo = lo.plane0[col] + (int64_t)(lo.nx - 1) * ctx->ps;
+    const double* src_hi = hi.plane0[col];
     if (lo.dev == s.dev)
       CK(cudaMemcpyAsync(g_lo, src_lo, face * 8, cudaMemcpyDeviceToDevice, s.stream));
     else
@@ -557,7 +569,7 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
                   colour_bytes, cudaGetErrorString(e));
     }
     CK(cudaMemset(s.buf[c], 0, colour_bytes));
-    s.plane0[c] = s.buf[c] + ctx->ps + ctx->org;
+    s.plane0[c] = s.buf[c] + ctx->ps;
     CK(cudaMalloc(&s.partials[c], (size_t)ctx->grid_cap * NTERMS * sizeof(double)));
   }
   if (ctx->d == 3) {
@@ -595,10 +607,8 @@ int init_geometry(kgs_ctx* ctx, int d, int64_t N, double a, double b) {
   ctx->nk = (int)(N / 2);
   ctx->ny = (d == 3) ? (int)N : 1;
   ctx->nxg = (d >= 2) ? N : 1;
-  ctx->rs = ctx->nk + 2 * GK;
-  ctx->gy = (d == 3) ? 1 : 0;
-  ctx->org = (int64_t)ctx->gy * ctx->rs + GK;
-  ctx->pp = (int64_t)(ctx->ny + 2 * ctx->gy) * ctx->rs;
+  ctx->rs = ctx->nk;
+  ctx->pp = (int64_t)ctx->ny * ctx->rs;
   ctx->ps = 4 * ctx->pp;
   return KGS_OK;
 }
@@ -777,8 +787,7 @@ int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
         PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
         g.own += fi * ctx->pp;
         g.oth += fi * ctx->pp;
-        split_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs,
-                                                  (ctx->d == 3 && fi < 3) ? 1 : 0);
+        split_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs);
         ctx->launches++;
         CK(cudaGetLastError());
       }
@@ -997,11 +1006,7 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
     switch (mode) {
       case 0: KGS_DBG(0) break;
       case 1: KGS_DBG(1) break;
-      case 2: KGS_DBG(2) break;
-      case 3: KGS_DBG(3) break;
-      case 4: KGS_DBG(4) break;
-      case 5: KGS_DBG(5) break;
-      default: KGS_DBG(6) break;
+      default: KGS_DBG(3) break;
     }
 #undef KGS_DBG
   }
@@ -1029,6 +1034,20 @@ int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatc
   cudaFree(d);
   if (e != cudaSuccess) return fail(nullptr, KGS_ECUDA, "division self-test: %s", cudaGetErrorString(e));
   *mismatches = (int64_t)h;
+  return KGS_OK;
+}
+
+int kgs_set_promotion(kgs_ctx* ctx, int halo, int tile) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  ctx->tune_promo_halo = halo;
+  ctx->tune_promo_tile = tile;
+  for (auto& s : ctx->slabs) {
+    if (ctx->d != 3) continue;
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.stream));
+    int r = make_tensor_maps(ctx, s);
+    if (r) return r;
+  }
   return KGS_OK;
 }
 
@@ -1064,7 +1083,7 @@ int kgs_fill_preset(kgs_ctx* ctx, int preset) {
     const int64_t n = (int64_t)s.nx * ctx->ny * ctx->nk * 2;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
     PassGeom g = make_geom(ctx, s, 0, 0, s.nx);   // own = black, oth = red
-    fill_preset<<<blocks, 256, 0, s.stream>>>(g, ctx->a, ctx->h, preset, ctx->d == 3 ? 1 : 0);
+    fill_preset<<<blocks, 256, 0, s.stream>>>(g, ctx->a, ctx->h, preset);
     ctx->launches++;
     CK(cudaGetLastError());
   }

@@ -21,7 +21,7 @@ pts = g.M // 2
 for v in map(int, a.variants.split(",")):
     for xc in (0,):
         dev.ctx.set_tuning(march_planes=xc, march_variant=v)
-        for mode in (0, 1, 2, 3, 4, 5, 6):
+        for mode in (0, 1, 3):
             ms = ctypes.c_double()
             _lib.check(_lib.load().kgs_debug_pass(dev.ctx.ptr, mode, 5, ctypes.byref(ms)),
                        dev.ctx.ptr)

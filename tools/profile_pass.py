@@ -14,10 +14,13 @@ ap.add_argument("--N", type=int, default=1024)
 ap.add_argument("--variant", type=int, default=1)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--xc", type=int, default=0)
+ap.add_argument("--promo", default="0,0")
 a = ap.parse_args()
 g = kgs.get_scenario("ellipsoids3d").default_grid(a.N)
 dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
 dev.ctx.set_tuning(march_planes=a.xc, march_variant=a.variant)
+ph, pt = map(int, a.promo.split(","))
+_lib.check(_lib.load().kgs_set_promotion(dev.ctx.ptr, ph, pt), dev.ctx.ptr)
 ms = ctypes.c_double()
 _lib.check(_lib.load().kgs_debug_pass(dev.ctx.ptr, a.mode, 1, ctypes.byref(ms)), dev.ctx.ptr)
 print(f"variant {a.variant} mode {a.mode}: {ms.value:.3f} ms")
