@@ -261,7 +261,11 @@ def run_ours(args):
     # e2e through the public API: integrate() on a pinned host state
     e2e = None
     if not args.no_e2e:
-        host = kgs.FieldState.pinned(g) if world == 1 else kgs.FieldState.zeros(g)
+        if world == 1:
+            host = kgs.FieldState.pinned(g)
+        else:   # each rank holds only its own slab on the host (32 GiB / world)
+            from paper_2502_09537_b200.device import pinned_empty
+            host = kgs.FieldState(*(pinned_empty(points_local) for _ in range(4)), 0.0)
         dev.download(host)
         dev.close()
         del dev

@@ -97,6 +97,15 @@ int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q,
 /* Device -> host copy of the owned planes (natural layout). */
 int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V);
 
+/* Plane-range transfers of ONE field (0 P, 1 Q, 2 U, 3 V): planes
+ * [x_begin, x_begin + nplanes) (global axis-0 indices inside this context's
+ * range), natural layout, nplanes * N^(d-1) doubles.  Used to stream KGS1
+ * snapshots (dpavf/snapshot.py:30-64) without a full host copy. */
+int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
+                      const double* src);
+int kgs_download_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
+                        double* dst);
+
 /* ---- the hot path ------------------------------------------------------ */
 
 /* One colour half of one sweep, in place: the device equivalent of
@@ -166,6 +175,11 @@ double kgs_last_step_ms(kgs_ctx* ctx);
  * rows x slots; < 0: keep).  Results do not depend on these (bitwise). */
 int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
                    int march_planes, int march_variant);
+
+/* Named tuning knob (results never depend on it): "march_variant",
+ * "march_planes", "march_sync" (planes between cluster barriers of the
+ * clustered variants), "blocks_per_sm".  KGS_EINVAL for unknown names. */
+int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 
 /* L2 sector promotion of the marching kernel's TMA boxes (0 none, 1 64 B,
  * 2 128 B, 3 256 B) for the other-colour halo box and the own tile box;

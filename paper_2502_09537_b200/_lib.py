@@ -32,7 +32,7 @@ EXPORTED = (
     "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version",
     "kgs_pass_timing", "kgs_pass_stats", "kgs_host_alloc", "kgs_host_free",
     "kgs_set_tuning", "kgs_selftest_division", "kgs_debug_pass",
-    "kgs_set_promotion",
+    "kgs_set_promotion", "kgs_set_param", "kgs_upload_planes", "kgs_download_planes",
 )
 
 
@@ -104,6 +104,9 @@ def load() -> ctypes.CDLL:
                                                  ctypes.POINTER(_I64)]),
         "kgs_debug_pass": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _DP]),
         "kgs_set_promotion": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
+        "kgs_set_param": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_int]),
+        "kgs_upload_planes": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _DP]),
+        "kgs_download_planes": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _DP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

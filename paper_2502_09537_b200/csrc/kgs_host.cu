@@ -71,8 +71,8 @@ struct Slab {
   int nx = 0;      // planes
   double* buf[2] = {nullptr, nullptr};    // colour c, ghost plane -1
   double* plane0[2] = {nullptr, nullptr}; // colour c, element (x=0,f=0,y=0,k=0)
-  MarchMaps maps[4][2];  // [march variant][colour]: TMA descriptors
-  bool has_tmaps[4] = {false, false, false, false};  // variant fits this geometry
+  MarchMaps maps[6][2];  // [march variant][colour]: TMA descriptors
+  bool has_tmaps[6] = {};  // variant fits this geometry
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
   double* records = nullptr;                 // device [cap * NTERMS]
@@ -108,6 +108,7 @@ struct kgs_ctx {
   int tune_xc = 0;  // march kernel planes per unit (0 auto, < 0 disables it)
   int tune_variant = 0;  // march kernel tile variant (MV0..MV3)
   int tune_promo_halo = 0, tune_promo_tile = 0;  // TMA L2 promotion (0 none .. 3 256B)
+  int tune_sync = 4;     // march clusters: planes between cluster barriers
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
   std::vector<cudaEvent_t> pass_ev;
@@ -232,9 +233,9 @@ EncodeTiledFn encode_tiled() {
 
 // 3-D march kernel variants: tile rows x slots, ring depths, min blocks/SM.
 // Larger tile cross-sections re-read fewer halo rows/slots.
-template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_>
+template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_, int CL_ = 1>
 struct MarchVariant {
-  static constexpr int TY = TY_, TK = TK_, NOTH = NOTH_, NOWN = NOWN_, MINB = MINB_;
+  static constexpr int TY = TY_, TK = TK_, NOTH = NOTH_, NOWN = NOWN_, MINB = MINB_, CL = CL_;
   static constexpr int NT = TY * TK;
   using L = MarchSmem<TY, TK, NOTH, NOWN>;
 };
@@ -242,9 +243,12 @@ using MV0 = MarchVariant<4, 64, 4, 2, 4>;     // 256 threads, 4 blocks/SM
 using MV1 = MarchVariant<8, 64, 4, 2, 2>;     // 512 threads, 2 blocks/SM
 using MV2 = MarchVariant<16, 32, 4, 2, 2>;    // 512 threads, 2 blocks/SM
 using MV3 = MarchVariant<32, 32, 4, 2, 1>;    // 1024 threads, 1 block/SM
-constexpr int kMarchVariants = 4;
-constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY};
-constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK};
+using MV4 = MarchVariant<4, 64, 4, 2, 4, 8>;  // MV0 in clusters of 8 along y
+using MV5 = MarchVariant<4, 64, 4, 2, 4, 4>;  // MV0 in clusters of 4 along y
+constexpr int kMarchVariants = 6;
+constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY, MV4::TY, MV5::TY};
+constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK, MV4::TK, MV5::TK};
+constexpr int kVarCL[kMarchVariants] = {MV0::CL, MV1::CL, MV2::CL, MV3::CL, MV4::CL, MV5::CL};
 
 // L2 sector promotion of the TMA boxes.  The two-slot halo columns are 16 B
 // inside a neighbouring tile's lines: promoting them to 256-B fetches would
@@ -271,7 +275,7 @@ int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
   const cuuint32_t es[4] = {1, 1, 1, 1};
   for (int v = 0; v < kMarchVariants; ++v) {
     const int ty = kVarTY[v], tk = kVarTK[v];
-    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % ty == 0 && ctx->nk % tk == 0 &&
+    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % (ty * kVarCL[v]) == 0 && ctx->nk % tk == 0 &&
                      ctx->nk >= 2 && (ctx->rs * 8) % 16 == 0;
     if (!s.has_tmaps[v]) continue;
     const cuuint32_t centre[4] = {(cuuint32_t)tk, 3, (cuuint32_t)ty, 1};
@@ -300,16 +304,34 @@ template <typename Var, int COL, int OP1, int OP2, bool DIAG, bool CHECK, int DB
 int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
                  int v) {
   using L = typename Var::L;
+  constexpr int CL = Var::CL;
   auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
-                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG>;
-  static int occ = 0;
+                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG, CL>;
+  static int occ = 0;  // resident CTAs per SM (or clusters per GPU / nsm when CL > 1)
+  static int max_clusters = 0;
   if (occ == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Var::NT, L::bytes));
     if (occ < 1) return fail(ctx, KGS_ECUDA, "march kernel does not fit on an SM");
+    if (CL > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(CL * 64);
+      cfg.blockDim = dim3(Var::NT);
+      cfg.dynamicSmemBytes = L::bytes;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+      if (max_clusters < 1) return fail(ctx, KGS_ECUDA, "march cluster does not fit");
+    }
   }
   const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
-  const int64_t G = std::min<int64_t>((int64_t)bps * ctx->nsm, ctx->grid_cap);
+  int64_t G = std::min<int64_t>((int64_t)bps * ctx->nsm, ctx->grid_cap);
+  if (CL > 1) G = std::min<int64_t>(G, (int64_t)max_clusters * CL) / CL * CL;
   const int64_t cols = (int64_t)(g.ny / Var::TY) * (g.nk / Var::TK);
   const int nxr = g.xb - g.xa;
   MarchCfg mc;
@@ -318,10 +340,28 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
     mc.xc = (int)std::max<int64_t>(std::min<int64_t>(nxr, 8),
                                    std::min<int64_t>(nxr, (int64_t)nxr * cols / (8 * G)));
   mc.nunits = (int64_t)((nxr + mc.xc - 1) / mc.xc) * cols;
-  const int64_t grid = std::min<int64_t>(mc.nunits, G);
+  mc.sync = std::max(1, ctx->tune_sync);
+  const int64_t grid = std::min<int64_t>(mc.nunits, G) / CL * CL;
   if (grid < 1) return KGS_OK;
-  kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
-      s.maps[v][COL ^ 1], s.maps[v][COL], g, c, s.partials[COL], s.bad, step_no, mc);
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(Var::NT);
+    cfg.dynamicSmemBytes = L::bytes;
+    cfg.stream = s.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, s.maps[v][COL ^ 1], s.maps[v][COL], g, c, s.partials[COL],
+                          s.bad, step_no, mc));
+  } else {
+    kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
+        s.maps[v][COL ^ 1], s.maps[v][COL], g, c, s.partials[COL], s.bad, step_no, mc);
+  }
   ctx->launches++;
   if (DIAG) s.npart[COL] = (int)grid;
   CK(cudaGetLastError());
@@ -345,7 +385,9 @@ int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, 
     case 0: return launch_march<MV0, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
     case 1: return launch_march<MV1, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
     case 2: return launch_march<MV2, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    default: return launch_march<MV3, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 3: return launch_march<MV3, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 4: return launch_march<MV4, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    default: return launch_march<MV5, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
   }
 }
 
@@ -768,30 +810,68 @@ int kgs_local_range(kgs_ctx* ctx, int64_t* x0, int64_t* nx, int64_t* points) {
   return KGS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Move planes [xg0, xg0 + n) (global plane indices inside this context) of
+// field `fi` between a host array in natural layout (`host` = plane xg0) and
+// the colour-split device planes, through each slab's staging buffer.
+int transfer_planes(kgs_ctx* ctx, int fi, int64_t xg0, int64_t n, double* host, bool to_device) {
+  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
+  for (auto& s : ctx->slabs) {
+    const int64_t lo = std::max<int64_t>(xg0, s.x0), hi = std::min<int64_t>(xg0 + n, s.x0 + s.nx);
+    if (lo >= hi) continue;
+    CK(cudaSetDevice(s.dev));
+    for (int64_t xg = lo; xg < hi; xg += s.stage_planes) {
+      const int nxc = (int)std::min<int64_t>(s.stage_planes, hi - xg);
+      const int xs = (int)(xg - s.x0);
+      const int64_t cnt = (int64_t)nxc * ctx->ny * ctx->nk;
+      const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
+      PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
+      g.own += fi * ctx->pp;
+      g.oth += fi * ctx->pp;
+      double* h = host + (xg - xg0) * nat_plane;
+      const size_t bytes = (size_t)nxc * nat_plane * 8;
+      if (to_device) {
+        CK(cudaMemcpyAsync(s.stage, h, bytes, cudaMemcpyHostToDevice, s.stream));
+        split_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs);
+      } else {
+        merge_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs);
+      }
+      ctx->launches++;
+      CK(cudaGetLastError());
+      if (!to_device) CK(cudaMemcpyAsync(h, s.stage, bytes, cudaMemcpyDeviceToHost, s.stream));
+    }
+    CK(cudaStreamSynchronize(s.stream));
+  }
+  return KGS_OK;
+}
+
+int check_range(kgs_ctx* ctx, int field, int64_t xg0, int64_t n, const void* p) {
+  if (!ctx || !p) return fail(ctx, KGS_EINVAL, "NULL argument");
+  if (field < 0 || field > 3) return fail(ctx, KGS_EINVAL, "field must be 0..3 (P, Q, U, V)");
+  int64_t lo = ctx->slabs.front().x0, cnt = 0;
+  for (auto& s : ctx->slabs) cnt += s.nx;
+  if (n < 0 || xg0 < lo || xg0 + n > lo + cnt)
+    return fail(ctx, KGS_EINVAL, "planes [%lld, %lld) outside this context's [%lld, %lld)",
+                (long long)xg0, (long long)(xg0 + n), (long long)lo, (long long)(lo + cnt));
+  return KGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
                const double* V) {
   if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
   const double* f[4] = {P, Q, U, V};
-  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
-  const int64_t base_x = ctx->slabs.front().x0;
-  for (auto& s : ctx->slabs) {
-    CK(cudaSetDevice(s.dev));
-    for (int fi = 0; fi < 4; ++fi) {
-      for (int xs = 0; xs < s.nx; xs += s.stage_planes) {
-        const int nxc = std::min(s.stage_planes, s.nx - xs);
-        const double* src = f[fi] + (s.x0 - base_x + xs) * nat_plane;
-        CK(cudaMemcpyAsync(s.stage, src, (size_t)nxc * nat_plane * 8,
-                           cudaMemcpyHostToDevice, s.stream));
-        const int64_t n = (int64_t)nxc * ctx->ny * ctx->nk;
-        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
-        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
-        g.own += fi * ctx->pp;
-        g.oth += fi * ctx->pp;
-        split_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs);
-        ctx->launches++;
-        CK(cudaGetLastError());
-      }
-    }
+  int64_t x0, nx;
+  kgs_local_range(ctx, &x0, &nx, nullptr);
+  for (int fi = 0; fi < 4; ++fi) {
+    int r = transfer_planes(ctx, fi, x0, nx, const_cast<double*>(f[fi]), true);
+    if (r) return r;
   }
   int r = exchange(ctx, 0);
   if (!r) r = exchange(ctx, 1);
@@ -802,29 +882,30 @@ int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
 int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V) {
   if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
   double* f[4] = {P, Q, U, V};
-  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
-  const int64_t base_x = ctx->slabs.front().x0;
-  for (auto& s : ctx->slabs) {
-    CK(cudaSetDevice(s.dev));
-    for (int fi = 0; fi < 4; ++fi) {
-      for (int xs = 0; xs < s.nx; xs += s.stage_planes) {
-        const int nxc = std::min(s.stage_planes, s.nx - xs);
-        const int64_t n = (int64_t)nxc * ctx->ny * ctx->nk;
-        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16);
-        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
-        g.own += fi * ctx->pp;
-        g.oth += fi * ctx->pp;
-        merge_field<<<blocks, 256, 0, s.stream>>>(s.stage, g, nxc, xs);
-        ctx->launches++;
-        CK(cudaGetLastError());
-        double* dst = f[fi] + (s.x0 - base_x + xs) * nat_plane;
-        CK(cudaMemcpyAsync(dst, s.stage, (size_t)nxc * nat_plane * 8,
-                           cudaMemcpyDeviceToHost, s.stream));
-      }
-    }
-    CK(cudaStreamSynchronize(s.stream));
+  int64_t x0, nx;
+  kgs_local_range(ctx, &x0, &nx, nullptr);
+  for (int fi = 0; fi < 4; ++fi) {
+    int r = transfer_planes(ctx, fi, x0, nx, f[fi], false);
+    if (r) return r;
   }
   return KGS_OK;
+}
+
+int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
+                      const double* src) {
+  int r = check_range(ctx, field, x_begin, nplanes, src);
+  if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, const_cast<double*>(src), true);
+  if (!r && field < 3) r = exchange(ctx, 0);   // refresh faces (P, Q, U are halo fields)
+  if (!r && field < 3) r = exchange(ctx, 1);
+  if (!r) r = sync_all(ctx);
+  return r;
+}
+
+int kgs_download_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
+                        double* dst) {
+  int r = check_range(ctx, field, x_begin, nplanes, dst);
+  if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, dst, false);
+  return r;
 }
 
 int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c) {
@@ -991,7 +1072,7 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   Slab& s = ctx->slabs[0];
   PassGeom g = make_geom(ctx, s, 0, 0, s.nx);
   const int v = march_variant(ctx, s, g);
-  if (v != 0 && v != 1) return fail(ctx, KGS_EINVAL, "debug pass needs march variant 0 or 1");
+  if (v != 0 && v != 4) return fail(ctx, KGS_EINVAL, "debug pass needs march variant 0 or 4");
   Coeffs c{};
   CK(cudaSetDevice(s.dev));
   cudaEvent_t a, b;
@@ -1002,7 +1083,7 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
     if (i == 1) CK(cudaEventRecord(a, s.stream));
 #define KGS_DBG(M)                                                                       \
   r = (v == 0) ? launch_march<MV0, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v) \
-               : launch_march<MV1, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v);
+               : launch_march<MV4, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v);
     switch (mode) {
       case 0: KGS_DBG(0) break;
       case 1: KGS_DBG(1) break;
@@ -1048,6 +1129,17 @@ int kgs_set_promotion(kgs_ctx* ctx, int halo, int tile) {
     int r = make_tensor_maps(ctx, s);
     if (r) return r;
   }
+  return KGS_OK;
+}
+
+int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
+  if (!ctx || !name) return fail(ctx, KGS_EINVAL, "NULL argument");
+  const std::string n(name);
+  if (n == "march_sync") ctx->tune_sync = std::max(1, value);
+  else if (n == "march_variant") ctx->tune_variant = value;
+  else if (n == "march_planes") ctx->tune_xc = value;
+  else if (n == "blocks_per_sm") ctx->tune_occ = value;
+  else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }
 

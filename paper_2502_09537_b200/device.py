@@ -114,9 +114,28 @@ class DeviceContext:
         _lib.check(rc, self.ptr)
 
     def local(self, a: np.ndarray) -> np.ndarray:
-        if a.shape != (self.grid.M,):
-            raise ValueError(f"field has shape {a.shape}, grid needs ({self.grid.M},)")
-        return a[self.offset:self.offset + self.points]
+        """This context's planes of a host field: a whole-grid array is
+        sliced; a distributed rank may also pass just its own slab."""
+        if a.shape == (self.grid.M,):
+            return a[self.offset:self.offset + self.points]
+        if self.dist and a.shape == (self.points,):
+            return a
+        raise ValueError(f"field has shape {a.shape}, grid needs ({self.grid.M},)")
+
+    def upload_planes(self, field: int, x_begin: int, data: np.ndarray) -> None:
+        """Planes [x_begin, x_begin + n) of one field (0 P .. 3 V), natural layout."""
+        a = np.ascontiguousarray(data, dtype=np.float64)
+        n = a.size // self.plane
+        if n * self.plane != a.size:
+            raise ValueError("data is not a whole number of planes")
+        self.check(_lib.load().kgs_upload_planes(self.ptr, field, x_begin, n, _lib.dptr(a)))
+
+    def download_planes(self, field: int, x_begin: int, out: np.ndarray) -> None:
+        n = out.size // self.plane
+        if n * self.plane != out.size or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError("out must be a contiguous whole number of planes")
+        self.check(_lib.load().kgs_download_planes(self.ptr, field, x_begin, n,
+                                                   _lib.dptr(out)))
 
     def upload(self, s: FieldState) -> None:
         f = [np.ascontiguousarray(self.local(np.asarray(a, dtype=np.float64)))
@@ -194,6 +213,9 @@ class DeviceContext:
                    march_variant: int = -1) -> None:
         self.check(_lib.load().kgs_set_tuning(self.ptr, rows_per_tile, band_rows,
                                               blocks_per_sm, march_planes, march_variant))
+
+    def set_param(self, name: str, value: int) -> None:
+        self.check(_lib.load().kgs_set_param(self.ptr, name.encode(), int(value)))
 
     def pass_timing(self, enable: bool) -> None:
         self.check(_lib.load().kgs_pass_timing(self.ptr, int(enable)))

@@ -13,7 +13,7 @@ from paper_2502_09537_b200 import _lib  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--N", type=int, default=1024)
-ap.add_argument("--variants", default="0,1")
+ap.add_argument("--variants", default="0,4")
 a = ap.parse_args()
 g = kgs.get_scenario("ellipsoids3d").default_grid(a.N)
 dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--occ", default="0")
     ap.add_argument("--variant", default="1")
     ap.add_argument("--xc", default="0")
+    ap.add_argument("--sync", default="4")
     a = ap.parse_args()
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(a.N)
@@ -34,16 +35,18 @@ def main():
     ctx.step_dpavf2(args, 2)
     pts = g.M // 2
     res = []
-    for ty, band, occ, var, xc in itertools.product(
-            *(list(map(int, s.split(","))) for s in (a.ty, a.band, a.occ, a.variant, a.xc))):
+    for ty, band, occ, var, xc, sync in itertools.product(
+            *(list(map(int, s.split(","))) for s in (a.ty, a.band, a.occ, a.variant, a.xc,
+                                                     a.sync))):
         ctx.set_tuning(ty, band, occ, xc, var)
+        ctx.set_param("march_sync", sync)
         ctx.step_dpavf2(args, 1)
         ctx.pass_timing(True)
         ctx.step_dpavf2(args, a.steps)
         n, ms, _ = ctx.pass_stats()
         ctx.pass_timing(False)
         avg = ms / n
-        r = {"ty": ty, "band": band, "occ": occ, "variant": var, "xc": xc,
+        r = {"ty": ty, "band": band, "occ": occ, "variant": var, "xc": xc, "sync": sync,
              "pass_ms": round(avg, 4),
              "step_ms_est": round(2 * avg, 3),
              "GBs_44B": round(44 * 2 * pts / avg / 1e6, 1),
