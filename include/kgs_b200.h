@@ -128,10 +128,17 @@ int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c);
  * When record_stride > 0, the energy/mass term sums (see kgs_energy_terms)
  * of the state after every step n with n % record_stride == 0 are written,
  * in step order, to terms_out[r * KGS_NTERMS + q], r = 0, 1, ...
- * terms_out may be NULL when no step is recorded. */
+ * terms_out may be NULL when no step is recorded.
+ * flags & KGS_STEP_DEFER_TAIL: the red adjoint half of the last step (unless
+ * that step is recorded) is left pending in the context and fused into the
+ * next call's first pass when the coefficients are equal -- 2 instead of 3
+ * passes per step for step-at-a-time callers.  Results are bitwise the same;
+ * every other entry point applies a pending adjoint first, and the last
+ * step is then not checked for finiteness (step_dpavf2 does not check). */
+#define KGS_STEP_DEFER_TAIL 1
 int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
                     int64_t step_offset, int64_t record_stride,
-                    double* terms_out, int64_t* first_bad_step);
+                    double* terms_out, int64_t* first_bad_step, int flags);
 
 /* ---- diagnostics (dpavf/grid.py:152-187) ------------------------------- */
 

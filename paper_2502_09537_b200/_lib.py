@@ -22,6 +22,7 @@ KGS_ENCCL = -3
 KGS_ENONFINITE = -4
 KGS_ENOMEM = -5
 NTERMS = 8
+KGS_STEP_DEFER_TAIL = 1
 
 # Every symbol include/kgs_b200.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -85,7 +86,7 @@ def load() -> ctypes.CDLL:
         "kgs_sweep": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int,
                                      ctypes.POINTER(KgsCoeffs)]),
         "kgs_step_dpavf2": (ctypes.c_int, [_P, ctypes.POINTER(KgsCoeffs), _I64, _I64, _I64,
-                                           _DP, ctypes.POINTER(_I64)]),
+                                           _DP, ctypes.POINTER(_I64), ctypes.c_int]),
         "kgs_energy_terms": (ctypes.c_int, [_P, _DP]),
         "kgs_energy_mass": (ctypes.c_int, [_P, _D, _D, _D, _D, _DP, _DP]),
         "kgs_all_finite": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),

@@ -109,6 +109,10 @@ struct kgs_ctx {
   int tune_variant = 0;  // march kernel tile variant (MV0..MV3)
   int tune_promo_halo = 0, tune_promo_tile = 0;  // TMA L2 promotion (0 none .. 3 256B)
   int tune_sync = 4;     // march clusters: planes between cluster barriers
+  // deferred tail (KGS_STEP_DEFER_TAIL): the red adjoint of the last step is
+  // pending and fuses with the next call's head when the coefficients match
+  bool pending = false;
+  Coeffs pend_c{};
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
   std::vector<cudaEvent_t> pass_ev;
@@ -413,6 +417,7 @@ int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
     KGS_CASE(OP_BASE, OP_ADJ, false, true)
     KGS_CASE(OP_BASE, OP_ADJ, true, true)
   } else {  // K4: red adjoint(n) + base(n+1); tail: red adjoint(n)
+    KGS_CASE(OP_ADJ, OP_BASE, false, false)   // deferred tail fused into a head
     KGS_CASE(OP_ADJ, OP_BASE, false, true)
     KGS_CASE(OP_ADJ, OP_BASE, true, true)
     KGS_CASE(OP_ADJ, OP_NONE, false, true)
@@ -557,6 +562,15 @@ int finalize_record(kgs_ctx* ctx, int64_t slot, bool both) {
     CK(cudaGetLastError());
   }
   return KGS_OK;
+}
+
+// Apply a deferred red adjoint so the resident state is the reference's.
+int flush_pending(kgs_ctx* ctx) {
+  if (!ctx->pending) return KGS_OK;
+  ctx->pending = false;
+  int r = all_passes(ctx, 1, OP_ADJ, OP_NONE, false, false, ctx->pend_c, 0);
+  if (!r) r = exchange(ctx, 1);
+  return r;
 }
 
 int ensure_records(kgs_ctx* ctx, int64_t n) {
@@ -866,6 +880,7 @@ extern "C" {
 int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
                const double* V) {
   if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
+  ctx->pending = false;  // the whole state is replaced
   const double* f[4] = {P, Q, U, V};
   int64_t x0, nx;
   kgs_local_range(ctx, &x0, &nx, nullptr);
@@ -881,6 +896,7 @@ int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
 
 int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V) {
   if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
+  if (int r0 = flush_pending(ctx)) return r0;
   double* f[4] = {P, Q, U, V};
   int64_t x0, nx;
   kgs_local_range(ctx, &x0, &nx, nullptr);
@@ -894,6 +910,7 @@ int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V) {
 int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
                       const double* src) {
   int r = check_range(ctx, field, x_begin, nplanes, src);
+  if (!r) r = flush_pending(ctx);
   if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, const_cast<double*>(src), true);
   if (!r && field < 3) r = exchange(ctx, 0);   // refresh faces (P, Q, U are halo fields)
   if (!r && field < 3) r = exchange(ctx, 1);
@@ -904,6 +921,7 @@ int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
 int kgs_download_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
                         double* dst) {
   int r = check_range(ctx, field, x_begin, nplanes, dst);
+  if (!r) r = flush_pending(ctx);
   if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, dst, false);
   return r;
 }
@@ -913,7 +931,8 @@ int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c) {
   if (colour != 0 && colour != 1) return fail(ctx, KGS_EINVAL, "colour must be 0 or 1");
   if (kind != 0 && kind != 1) return fail(ctx, KGS_EINVAL, "kind must be 0 (base) or 1 (adjoint)");
   const Coeffs k = to_coeffs(c);
-  int r = all_passes(ctx, colour, kind == 0 ? OP_BASE : OP_ADJ, OP_NONE, false, false, k, 0);
+  int r = flush_pending(ctx);
+  if (!r) r = all_passes(ctx, colour, kind == 0 ? OP_BASE : OP_ADJ, OP_NONE, false, false, k, 0);
   if (!r) r = exchange(ctx, colour);
   if (!r) r = sync_all(ctx);
   return r;
@@ -921,7 +940,7 @@ int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c) {
 
 int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
                     int64_t step_offset, int64_t record_stride,
-                    double* terms_out, int64_t* first_bad_step) {
+                    double* terms_out, int64_t* first_bad_step, int flags) {
   if (!ctx || !half) return fail(ctx, KGS_EINVAL, "NULL argument");
   if (nsteps < 0 || record_stride < 0 || step_offset < 0)
     return fail(ctx, KGS_EINVAL, "negative nsteps/step_offset/record_stride");
@@ -939,9 +958,19 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
     CK(cudaSetDevice(s.dev));
     CK(cudaEventRecord(s.ev_t0, s.stream));
   }
-  // head: base red(first step)
-  r = all_passes(ctx, 1, OP_BASE, OP_NONE, false, false, c, 0);
+  // head: base red(first step) -- fused with a deferred red adjoint of the
+  // previous call when its coefficients are the same (bitwise neutral)
+  if (ctx->pending && std::memcmp(&ctx->pend_c, &c, sizeof c) == 0) {
+    ctx->pending = false;
+    r = all_passes(ctx, 1, OP_ADJ, OP_BASE, false, false, c, 0);
+  } else {
+    r = flush_pending(ctx);
+    if (!r) r = all_passes(ctx, 1, OP_BASE, OP_NONE, false, false, c, 0);
+  }
   if (!r) r = exchange(ctx, 1);
+  const int64_t last = step_offset + nsteps;
+  const bool defer = (flags & KGS_STEP_DEFER_TAIL) &&
+                     !(record_stride > 0 && last % record_stride == 0);
   int64_t slot = 0;
   for (int64_t i = 1; i <= nsteps && !r; ++i) {
     const int64_t n = step_offset + i;
@@ -951,7 +980,11 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
     if (!r) r = exchange(ctx, 0);
     // K4: red adjoint(n) + base(n+1), or the tail: red adjoint(last)
     if (!r && i < nsteps) r = timed_passes(ctx, 1, OP_ADJ, OP_BASE, rec, true, c, (int)n);
-    else if (!r) r = all_passes(ctx, 1, OP_ADJ, OP_NONE, rec, true, c, (int)n);
+    else if (!r && defer) {  // leave the red adjoint of the last step pending
+      ctx->pending = true;
+      ctx->pend_c = c;
+      break;
+    } else if (!r) r = all_passes(ctx, 1, OP_ADJ, OP_NONE, rec, true, c, (int)n);
     if (!r) r = exchange(ctx, 1);
     if (!r && rec) r = finalize_record(ctx, slot++, true);
   }
@@ -993,7 +1026,8 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
 int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
   if (!ctx || !terms_out) return fail(ctx, KGS_EINVAL, "NULL argument");
   Coeffs dummy{};
-  int r = ensure_records(ctx, 1);
+  int r = flush_pending(ctx);
+  if (!r) r = ensure_records(ctx, 1);
   // red: edges + red self terms; black: black self terms
   if (!r) r = all_passes(ctx, 1, OP_NONE, OP_NONE, true, false, dummy, 0);
   if (!r) r = all_passes(ctx, 0, OP_NONE, OP_NONE, true, false, dummy, 0);
@@ -1028,7 +1062,8 @@ int kgs_energy_mass(kgs_ctx* ctx, double kappa1, double kappa2, double mu,
 int kgs_all_finite(kgs_ctx* ctx, int* ok) {
   if (!ctx || !ok) return fail(ctx, KGS_EINVAL, "NULL argument");
   Coeffs dummy{};
-  int r = reset_bad(ctx);
+  int r = flush_pending(ctx);
+  if (!r) r = reset_bad(ctx);
   if (!r) r = all_passes(ctx, 1, OP_NONE, OP_NONE, false, true, dummy, 1);
   if (!r) r = all_passes(ctx, 0, OP_NONE, OP_NONE, false, true, dummy, 1);
   if (!r) r = sync_all(ctx);
@@ -1073,6 +1108,7 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   PassGeom g = make_geom(ctx, s, 0, 0, s.nx);
   const int v = march_variant(ctx, s, g);
   if (v != 0 && v != 4) return fail(ctx, KGS_EINVAL, "debug pass needs march variant 0 or 4");
+  if (int r0 = flush_pending(ctx)) return r0;
   Coeffs c{};
   CK(cudaSetDevice(s.dev));
   cudaEvent_t a, b;
@@ -1165,6 +1201,7 @@ int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
 
 int kgs_fill_preset(kgs_ctx* ctx, int preset) {
   if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  ctx->pending = false;  // the whole state is replaced
   const int need_d[4] = {3, 2, 2, 1};
   if (preset < 0 || preset > 3) return fail(ctx, KGS_EINVAL, "unknown preset %d", preset);
   if (need_d[preset] != ctx->d)

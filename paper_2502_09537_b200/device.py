@@ -174,8 +174,9 @@ class DeviceContext:
         self.check(_lib.load().kgs_sweep(self.ptr, colour, kind, ctypes.byref(c)))
 
     def step_dpavf2(self, kernel_args, nsteps: int, step_offset: int = 0,
-                    record_stride: int = 0):
-        """Run nsteps fused DP-AVF2 steps; returns (terms[nrec, 8], bad_step)."""
+                    record_stride: int = 0, defer_tail: bool = False):
+        """Run nsteps fused DP-AVF2 steps; returns (terms[nrec, 8], bad_step).
+        defer_tail: leave the last red adjoint pending (see kgs_b200.h)."""
         lib = _lib.load()
         c = _lib.coeffs_struct(kernel_args)
         if record_stride > 0:
@@ -185,7 +186,8 @@ class DeviceContext:
         terms = np.zeros((max(nrec, 1), _lib.NTERMS))
         bad = ctypes.c_int64(0)
         rc = lib.kgs_step_dpavf2(self.ptr, ctypes.byref(c), nsteps, step_offset,
-                                 record_stride, _lib.dptr(terms), ctypes.byref(bad))
+                                 record_stride, _lib.dptr(terms), ctypes.byref(bad),
+                                 _lib.KGS_STEP_DEFER_TAIL if defer_tail else 0)
         if rc not in (_lib.KGS_OK, _lib.KGS_ENONFINITE):
             self.check(rc)
         bad_step = bad.value if rc == _lib.KGS_ENONFINITE else 0

@@ -111,7 +111,9 @@ def step_dpavf2(state, schedule, coeffs_half: StepCoefficients, executor,
         step_adjoint(state, schedule, coeffs_half, executor, grid)
         return
     dev, temp = as_device_state(state, grid, executor)
-    _, bad = dev.ctx.step_dpavf2(coeffs_half.kernel_args(), 1)
+    # resident states defer the last red adjoint into the next call's head
+    # (2 passes per step instead of 3; bitwise neutral, see kgs_b200.h)
+    dev.ctx.step_dpavf2(coeffs_half.kernel_args(), 1, defer_tail=not temp)
     if temp:
         dev.ctx.download(state)
     state.t += coeffs_half.tau

@@ -240,3 +240,34 @@ def test_march_kernel_matches_simple_kernel(variant, xc):
         dev.close()
     assert_bitwise(outs[0][0], outs[1][0])
     np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-13)
+
+
+def test_step_at_a_time_with_deferred_tail_is_bitwise(golden):
+    """Resident step_dpavf2 calls defer the last red adjoint into the next
+    call's head; any later access (energy, download, sweep, coefficient
+    change) sees exactly the reference state."""
+    c = golden.case("d3_rand_N8")
+    coeffs = kgs.precompute_coefficients(c.params, c.meta["tau"] / 2.0, c.grid)
+    sch = kgs.checkerboard_schedule(c.grid)
+    dev = kgs.DeviceFieldState.from_host(c.state(0), c.grid)
+    ref = c.state(0)
+    for k in range(1, 8):
+        kgs.step_dpavf2(dev, sch, coeffs, None, c.grid)
+        oracle.numpy_step_dpavf2(ref, c.kernel_args, c.grid)
+        if k in (3, 7):
+            assert_bitwise(dev.to_host(), ref)
+            e = kgs.discrete_energy(dev, c.params, c.grid)
+            assert e == pytest.approx(oracle.discrete_energy(ref, c.params, c.grid), rel=1e-13)
+    # different coefficients after a deferred step: flush, then a fresh head
+    other = kgs.precompute_coefficients(c.params, c.meta["tau"], c.grid)
+    kgs.step_dpavf2(dev, sch, other, None, c.grid)
+    oracle.numpy_step_dpavf2(ref, oracle.kernel_args(c.params, c.meta["tau"], c.grid), c.grid)
+    assert_bitwise(dev.to_host(), ref)
+    # a single sweep after a deferred step
+    kgs.step_dpavf2(dev, sch, coeffs, None, c.grid)
+    kgs.step_base(dev, sch, coeffs, None, c.grid)
+    oracle.numpy_step_dpavf2(ref, c.kernel_args, c.grid)
+    for colour in (1, 0):
+        oracle.numpy_half_sweep(ref, c.kernel_args, c.grid, colour, False)
+    assert_bitwise(dev.to_host(), ref)
+    dev.close()
