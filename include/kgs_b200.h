@@ -185,7 +185,10 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
 
 /* Named tuning knob (results never depend on it): "march_variant",
  * "march_planes", "march_sync" (planes between cluster barriers of the
- * clustered variants), "blocks_per_sm".  KGS_EINVAL for unknown names. */
+ * clustered variants), "blocks_per_sm", "fused_sweep" (1: one fused sweep
+ * per DP-AVF2 step when the geometry allows -- experimental, bitwise equal
+ * but currently slower; 0, the default: two colour passes).
+ * KGS_EINVAL for unknown names. */
 int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 
 /* L2 sector promotion of the marching kernel's TMA boxes (0 none, 1 64 B,
@@ -204,11 +207,12 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out);
  * counts bitwise differences (expected 0). */
 int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatches);
 
-/* Per-launch timing of the fused colour passes (K3 black base+adjoint and
- * K4 red adjoint+base) inside kgs_step_dpavf2: when enabled, a CUDA event
- * pair brackets each such launch on its stream.  kgs_pass_stats returns the
+/* Per-launch timing of the fused launches inside kgs_step_dpavf2 (colour
+ * passes K3 / K4, or one-sweep steps): when enabled, a CUDA event pair
+ * brackets each such launch on its stream.  kgs_pass_stats returns the
  * number of timed launches and their summed device time (ms) since the
- * last kgs_pass_timing call, and the points each launch updated (twice). */
+ * last kgs_pass_timing call, and the points each launch updated twice
+ * (one colour for a pass, the whole grid for a sweep). */
 int kgs_pass_timing(kgs_ctx* ctx, int enable);
 int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
                    int64_t* points_per_launch);

@@ -73,6 +73,8 @@ struct Slab {
   double* plane0[2] = {nullptr, nullptr}; // colour c, element (x=0,f=0,y=0,k=0)
   MarchMaps maps[6][2];  // [march variant][colour]: TMA descriptors
   bool has_tmaps[6] = {};  // variant fits this geometry
+  int* prog = nullptr;     // fused sweep: K3 progress per column
+  int64_t prog_cap = 0;
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
   double* records = nullptr;                 // device [cap * NTERMS]
@@ -113,6 +115,9 @@ struct kgs_ctx {
   // pending and fuses with the next call's head when the coefficients match
   bool pending = false;
   Coeffs pend_c{};
+  int tune_sweep = 0;      // fused one-sweep DP-AVF2 steps (experimental, opt-in)
+  int tune_sweep_dbg = 0;  // timing experiments only (results invalid)
+  int64_t timed_pts = 0;   // points updated twice per timed launch
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
   std::vector<cudaEvent_t> pass_ev;
@@ -372,6 +377,60 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   return KGS_OK;
 }
 
+// ---- fused step sweep (variant 0 tiles) ----------------------------------
+constexpr size_t kSweepSmem = SweepSmem<MV0::TY, MV0::TK>::bytes;
+
+bool sweep_eligible(const kgs_ctx* ctx, const Slab& s) {
+  return ctx->tune_sweep && ctx->tune_xc >= 0 && ctx->d == 3 && ctx->slabs.size() == 1 &&
+         !(ctx->dist && ctx->nranks > 1) && s.has_tmaps[0] && s.nx >= 4;
+}
+
+template <bool DIAG, int K4OP2>
+int launch_sweep(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no) {
+  constexpr int MINB = DIAG ? 1 : 2;
+  auto kern = sweep_pass<DIAG, K4OP2, MV0::TY, MV0::TK, MINB>;
+  static int occ = 0;
+  if (occ == 0) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MV0::NT, kSweepSmem));
+    if (occ < 1) return fail(ctx, KGS_ECUDA, "sweep kernel does not fit on an SM");
+  }
+  const int nkt = ctx->nk / MV0::TK, nyt = ctx->ny / MV0::TY;
+  SweepCfg sc;
+  sc.ncols = nkt * nyt;
+  sc.D = 3 * nkt;
+  sc.nunits = (int64_t)sc.ncols + sc.D;
+  sc.dbg = ctx->tune_sweep_dbg;
+  if (s.prog_cap < sc.ncols) {
+    if (s.prog) CK(cudaFree(s.prog));
+    s.prog = nullptr;
+    CK(cudaMalloc(&s.prog, (size_t)sc.ncols * sizeof(int)));
+    s.prog_cap = sc.ncols;
+  }
+  CK(cudaMemsetAsync(s.prog, 0, (size_t)sc.ncols * sizeof(int), s.stream));
+  // persistent grid no larger than the co-resident capacity: the progress
+  // waits point only to earlier units, which is deadlock-free only if every
+  // launched block is resident
+  const int64_t grid = std::min<int64_t>({sc.nunits, (int64_t)occ * ctx->nsm, ctx->grid_cap});
+  PassGeom gb = make_geom(ctx, s, 0, 0, s.nx), gr = make_geom(ctx, s, 1, 0, s.nx);
+  kern<<<(unsigned)grid, MV0::NT, kSweepSmem, s.stream>>>(
+      s.maps[0][1], s.maps[0][0], gb, gr, c, s.partials[0], s.partials[1], s.bad, step_no,
+      s.prog, sc);
+  ctx->launches++;
+  if (DIAG) { s.npart[0] = (int)grid; s.npart[1] = (int)grid; }
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+int sweep_step(kgs_ctx* ctx, bool diag, bool last, const Coeffs& c, int step_no) {
+  Slab& s = ctx->slabs[0];
+  CK(cudaSetDevice(s.dev));
+  if (diag) return last ? launch_sweep<true, OP_NONE>(ctx, s, c, step_no)
+                        : launch_sweep<true, OP_BASE>(ctx, s, c, step_no);
+  return last ? launch_sweep<false, OP_NONE>(ctx, s, c, step_no)
+              : launch_sweep<false, OP_BASE>(ctx, s, c, step_no);
+}
+
 // march variant to use for this pass, or -1 for the simple kernel
 int march_variant(const kgs_ctx* ctx, const Slab& s, const PassGeom& g) {
   if (ctx->d != 3 || ctx->tune_xc < 0 || g.xb - g.xa < 1) return -1;
@@ -517,9 +576,37 @@ int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
   return KGS_OK;
 }
 
+// Run `launch` bracketed by an event pair on slab 0's stream when timing.
+template <class F>
+int timed(kgs_ctx* ctx, int64_t pts, F&& launch) {
+  ctx->timed_pts = pts;
+  if (!ctx->pass_timing) return launch();
+  Slab& s0 = ctx->slabs[0];
+  if (ctx->pass_ev_used + 2 > ctx->pass_ev.size()) {
+    CK(cudaSetDevice(s0.dev));
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->pass_ev.push_back(e);
+    }
+  }
+  cudaEvent_t a = ctx->pass_ev[ctx->pass_ev_used++];
+  cudaEvent_t b = ctx->pass_ev[ctx->pass_ev_used++];
+  CK(cudaSetDevice(s0.dev));
+  CK(cudaEventRecord(a, s0.stream));
+  int r = launch();
+  if (r) return r;
+  CK(cudaSetDevice(s0.dev));
+  CK(cudaEventRecord(b, s0.stream));
+  return KGS_OK;
+}
+
 // all_passes() bracketed by an event pair on slab 0's stream when timing.
 int timed_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
                  const Coeffs& c, int step_no) {
+  int64_t pts = 0;
+  for (auto& s : ctx->slabs) pts += (int64_t)s.nx * ctx->ny * ctx->nk;
+  ctx->timed_pts = pts;
   if (!ctx->pass_timing) return all_passes(ctx, col, op1, op2, diag, check, c, step_no);
   Slab& s0 = ctx->slabs[0];
   if (ctx->pass_ev_used + 2 > ctx->pass_ev.size()) {
@@ -805,6 +892,7 @@ int kgs_destroy(kgs_ctx* ctx) {
     if (s.records) cudaFree(s.records);
     if (s.bad) cudaFree(s.bad);
     if (s.stage) cudaFree(s.stage);
+    if (s.prog) cudaFree(s.prog);
     if (s.ev_done) cudaEventDestroy(s.ev_done);
     if (s.ev_t0) cudaEventDestroy(s.ev_t0);
     if (s.ev_t1) cudaEventDestroy(s.ev_t1);
@@ -972,9 +1060,17 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
   const bool defer = (flags & KGS_STEP_DEFER_TAIL) &&
                      !(record_stride > 0 && last % record_stride == 0);
   int64_t slot = 0;
+  const bool sweep = sweep_eligible(ctx, ctx->slabs[0]);
   for (int64_t i = 1; i <= nsteps && !r; ++i) {
     const int64_t n = step_offset + i;
     const bool rec = record_stride > 0 && n % record_stride == 0;
+    if (sweep && !(i == nsteps && defer)) {
+      // one fused sweep: K3(n) and K4(n) (the tail adjoint on the last step)
+      const int64_t pts = (int64_t)ctx->slabs[0].nx * ctx->ny * ctx->nk * 2;
+      r = timed(ctx, pts, [&] { return sweep_step(ctx, rec, i == nsteps, c, (int)n); });
+      if (!r && rec) r = finalize_record(ctx, slot++, true);
+      continue;
+    }
     // K3: black base(n) + adjoint(n)
     r = timed_passes(ctx, 0, OP_BASE, OP_ADJ, rec, true, c, (int)n);
     if (!r) r = exchange(ctx, 0);
@@ -1175,6 +1271,8 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "march_variant") ctx->tune_variant = value;
   else if (n == "march_planes") ctx->tune_xc = value;
   else if (n == "blocks_per_sm") ctx->tune_occ = value;
+  else if (n == "fused_sweep") ctx->tune_sweep = value;
+  else if (n == "sweep_debug") ctx->tune_sweep_dbg = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }
@@ -1193,9 +1291,7 @@ int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
   if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
   if (launches) *launches = ctx->pass_count;
   if (total_ms) *total_ms = ctx->pass_ms;
-  int64_t pts = 0;
-  for (auto& s : ctx->slabs) pts += (int64_t)s.nx * ctx->ny * ctx->nk;  // one colour
-  if (points_per_launch) *points_per_launch = pts;
+  if (points_per_launch) *points_per_launch = ctx->timed_pts;
   return KGS_OK;
 }
 

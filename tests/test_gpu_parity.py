@@ -271,3 +271,50 @@ def test_step_at_a_time_with_deferred_tail_is_bitwise(golden):
         oracle.numpy_half_sweep(ref, c.kernel_args, c.grid, colour, False)
     assert_bitwise(dev.to_host(), ref)
     dev.close()
+
+
+@pytest.mark.parametrize("N,steps,stride", [(128, 7, 3), (256, 4, 4), (128, 1, 1)])
+def test_fused_sweep_matches_two_pass_and_oracle(N, steps, stride):
+    """One fused sweep per step (K3 + lagged K4 with progress flags) gives the
+    same bits as two colour passes, the same energy records, and (128^3) the
+    same bits as the C oracle of the reference algorithm."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(N)
+    s0 = sc.state(g) if N <= 128 else None
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    outs = []
+    for fused in (0, 1):
+        dev = (kgs.DeviceFieldState.from_host(s0, g) if s0 is not None
+               else kgs.DeviceFieldState.from_preset("ellipsoids3d", g))
+        dev.ctx.set_param("fused_sweep", fused)
+        terms, bad = dev.ctx.step_dpavf2(args, steps, 0, stride)
+        assert bad == 0
+        outs.append((dev.to_host(), terms))
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-13)
+    if s0 is not None:
+        ref = s0.copy()
+        oracle.CheckerboardOracle(3, N).step_dpavf2(
+            ref, args, steps, workers=oracle.CheckerboardOracle.max_threads())
+        assert_bitwise(outs[1][0], ref)
+
+
+def test_fused_sweep_deferred_tail_and_nonfinite():
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    coeffs = kgs.precompute_coefficients(sc.params, 0.005, g)
+    sch = kgs.checkerboard_schedule(g)
+    dev = kgs.DeviceFieldState.from_host(s0, g)
+    ref = s0.copy()
+    for _ in range(3):
+        kgs.step_dpavf2(dev, sch, coeffs, None, g)
+    oracle.CheckerboardOracle(3, 128).step_dpavf2(ref, coeffs.kernel_args(), 3, workers=8)
+    assert_bitwise(dev.to_host(), ref)
+    bad = s0.copy()
+    bad.U[12345] = np.inf
+    dev.upload(bad)
+    _, first_bad = dev.ctx.step_dpavf2(coeffs.kernel_args(), 3, 0, 0)
+    assert first_bad == 1
+    dev.close()
