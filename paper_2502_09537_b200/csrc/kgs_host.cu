@@ -82,8 +82,12 @@ struct Slab {
   unsigned long long* bad = nullptr;
   double* stage = nullptr;  // natural-layout staging planes
   int stage_planes = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;    // compute
+  cudaStream_t cstream = nullptr;   // halo exchange (copies / NCCL)
   cudaEvent_t ev_done = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  cudaEvent_t ev_bnd = nullptr;     // boundary planes of the last pass written
+  cudaEvent_t ev_xch = nullptr;     // last exchange into this slab's ghosts done
+  bool xch_pending = false;
 };
 
 }  // namespace
@@ -214,10 +218,10 @@ int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
   int64_t grid = std::min<int64_t>(g.ntiles, (int64_t)bps * ctx->nsm);
   grid = std::min<int64_t>(grid, ctx->grid_cap);
   if (grid < 1) return KGS_OK;  // nothing to do
-  kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(g, c, s.partials[COL], s.bad,
-                                                  step_no);
+  kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(
+      g, c, s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no);
   ctx->launches++;
-  if (DIAG) s.npart[COL] = (int)grid;
+  if (DIAG) s.npart[COL] += (int)grid;
   CK(cudaGetLastError());
   return KGS_OK;
 }
@@ -365,14 +369,16 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
     cfg.stream = s.stream;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, s.maps[v][COL ^ 1], s.maps[v][COL], g, c, s.partials[COL],
-                          s.bad, step_no, mc));
+    CK(cudaLaunchKernelEx(&cfg, kern, s.maps[v][COL ^ 1], s.maps[v][COL], g, c,
+                          s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no,
+                          mc));
   } else {
     kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
-        s.maps[v][COL ^ 1], s.maps[v][COL], g, c, s.partials[COL], s.bad, step_no, mc);
+        s.maps[v][COL ^ 1], s.maps[v][COL], g, c,
+        s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no, mc);
   }
   ctx->launches++;
-  if (DIAG) s.npart[COL] = (int)grid;
+  if (DIAG) s.npart[COL] += (int)grid;
   CK(cudaGetLastError());
   return KGS_OK;
 }
@@ -488,8 +494,8 @@ int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
 }
 
 int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
-                bool check, const Coeffs& c, int step_no) {
-  PassGeom g = make_geom(ctx, s, col, 0, s.nx);
+                bool check, const Coeffs& c, int step_no, int xa = 0, int xb = -1) {
+  PassGeom g = make_geom(ctx, s, col, xa, xb < 0 ? s.nx : xb);
   switch (ctx->d * 2 + col) {
     case 2: return launch_col<1, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
     case 3: return launch_col<1, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
@@ -504,56 +510,74 @@ int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
 // ---- halo exchange of colour `col` faces (P, Q, U of planes 0 and nx-1) --
 // The three fields of a plane are contiguous ([P|Q|U|V] per plane), so a
 // face is ONE contiguous run of 3*pp doubles.
+bool needs_exchange(const kgs_ctx* ctx) {
+  return ctx->dist ? ctx->nranks > 1 : ctx->slabs.size() > 1;
+}
+
+// Start the exchange of colour `col` faces (P, Q, U of planes 0 and nx-1)
+// on each slab's comm stream, after the boundary planes of the pass that
+// wrote them (ev_bnd); completion is ev_xch, which the next pass waits for
+// only before ITS boundary planes -- the interior planes overlap the
+// transfer.  The three fields of a plane are contiguous ([P|Q|U|V] per
+// plane), so a face is ONE contiguous run of 3*pp doubles.
 int exchange(kgs_ctx* ctx, int col) {
+  if (!needs_exchange(ctx)) return KGS_OK;  // a single slab wraps in the kernel
   const size_t face = (size_t)3 * ctx->pp;
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaEventRecord(s.ev_bnd, s.stream));
+  }
   if (ctx->dist) {
-    if (ctx->nranks == 1) return KGS_OK;
     Slab& s = ctx->slabs[0];
     const int up = (ctx->rank + 1) % ctx->nranks;
     const int dn = (ctx->rank - 1 + ctx->nranks) % ctx->nranks;
     double* p0 = s.plane0[col];
+    CK(cudaStreamWaitEvent(s.cstream, s.ev_bnd, 0));
     NK(g_nccl.GroupStart());
     // order matters when up == dn (2 ranks): sends [to dn: plane 0, to up:
     // plane nx-1]; recvs [from up: ghost nx, from dn: ghost -1].
-    NK(g_nccl.Send(p0, face, ncclFloat64, dn, ctx->comm, s.stream));
+    NK(g_nccl.Send(p0, face, ncclFloat64, dn, ctx->comm, s.cstream));
     NK(g_nccl.Send(p0 + (int64_t)(s.nx - 1) * ctx->ps, face, ncclFloat64, up,
-                   ctx->comm, s.stream));
+                   ctx->comm, s.cstream));
     NK(g_nccl.Recv(p0 + (int64_t)s.nx * ctx->ps, face, ncclFloat64, up,
-                   ctx->comm, s.stream));
-    NK(g_nccl.Recv(p0 - ctx->ps, face, ncclFloat64, dn, ctx->comm, s.stream));
+                   ctx->comm, s.cstream));
+    NK(g_nccl.Recv(p0 - ctx->ps, face, ncclFloat64, dn, ctx->comm, s.cstream));
     NK(g_nccl.GroupEnd());
+    CK(cudaEventRecord(s.ev_xch, s.cstream));
+    s.xch_pending = true;
     return KGS_OK;
   }
   const int ns = (int)ctx->slabs.size();
-  if (ns == 1) return KGS_OK;  // single slab wraps inside the kernel
-  for (auto& s : ctx->slabs) {
-    CK(cudaSetDevice(s.dev));
-    CK(cudaEventRecord(s.ev_done, s.stream));
-  }
   for (int i = 0; i < ns; ++i) {
     Slab& s = ctx->slabs[i];
     Slab& lo = ctx->slabs[(i - 1 + ns) % ns];
     Slab& hi = ctx->slabs[(i + 1) % ns];
     CK(cudaSetDevice(s.dev));
-    CK(cudaStreamWaitEvent(s.stream, lo.ev_done, 0));
-    CK(cudaStreamWaitEvent(s.stream, hi.ev_done, 0));
+    // own boundary pass done (it read these ghosts' previous contents) and
+    // the neighbours' faces written
+    CK(cudaStreamWaitEvent(s.cstream, s.ev_bnd, 0));
+    CK(cudaStreamWaitEvent(s.cstream, lo.ev_bnd, 0));
+    CK(cudaStreamWaitEvent(s.cstream, hi.ev_bnd, 0));
     // pull: ghost -1 <- lo plane nx-1 ; ghost nx <- hi plane 0
     double* g_lo = s.plane0[col] - ctx->ps;
     double* g_hi = s.plane0[col] + (int64_t)s.nx * ctx->ps;
     const double* src_lo = lo.plane0[col] + (int64_t)(lo.nx - 1) * ctx->ps;
     const double* src_hi = hi.plane0[col];
     if (lo.dev == s.dev)
-      CK(cudaMemcpyAsync(g_lo, src_lo, face * 8, cudaMemcpyDeviceToDevice, s.stream));
+      CK(cudaMemcpyAsync(g_lo, src_lo, face * 8, cudaMemcpyDeviceToDevice, s.cstream));
     else
-      CK(cudaMemcpyPeerAsync(g_lo, s.dev, src_lo, lo.dev, face * 8, s.stream));
+      CK(cudaMemcpyPeerAsync(g_lo, s.dev, src_lo, lo.dev, face * 8, s.cstream));
     if (hi.dev == s.dev)
-      CK(cudaMemcpyAsync(g_hi, src_hi, face * 8, cudaMemcpyDeviceToDevice, s.stream));
+      CK(cudaMemcpyAsync(g_hi, src_hi, face * 8, cudaMemcpyDeviceToDevice, s.cstream));
     else
-      CK(cudaMemcpyPeerAsync(g_hi, s.dev, src_hi, hi.dev, face * 8, s.stream));
+      CK(cudaMemcpyPeerAsync(g_hi, s.dev, src_hi, hi.dev, face * 8, s.cstream));
+    CK(cudaEventRecord(s.ev_xch, s.cstream));
+    s.xch_pending = true;
   }
-  // the next pass on slab i must not overwrite colour `col` planes that a
-  // neighbour is still pulling: the pass after next (same colour) is ordered
-  // behind the neighbour's pulls via the next exchange's event waits.
+  // A face read by a neighbour's pull in exchange k is next overwritten by
+  // this slab's boundary pass k+2, which waits for this slab's exchange k+1,
+  // which waits (ev_bnd) for the neighbour's boundary pass k+1, which waits
+  // for the neighbour's exchange k: ordered.
   return KGS_OK;
 }
 
@@ -561,16 +585,35 @@ int sync_all(kgs_ctx* ctx) {
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamSynchronize(s.stream));
+    CK(cudaStreamSynchronize(s.cstream));
   }
   return KGS_OK;
 }
 
+// One colour pass over every slab.  With several slabs (or ranks) the
+// interior planes [1, nx-1) go first -- they need no ghost data, so they
+// overlap the previous pass's halo exchange -- then the stream waits for
+// that exchange (ev_xch) and runs the two boundary planes.
 int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
                const Coeffs& c, int step_no) {
+  const bool split = needs_exchange(ctx);
   for (auto& s : ctx->slabs) {
     cudaError_t e = cudaSetDevice(s.dev);
     if (e != cudaSuccess) return fail(ctx, KGS_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
-    int r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no);
+    if (diag) s.npart[col] = 0;
+    int r;
+    if (!split) {
+      r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no);
+    } else {
+      r = KGS_OK;
+      if (s.nx > 2) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, 1, s.nx - 1);
+      if (!r && s.xch_pending) {
+        CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+        s.xch_pending = false;
+      }
+      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, 0, 1);
+      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, s.nx - 1, s.nx);
+    }
     if (r) return r;
   }
   return KGS_OK;
@@ -713,7 +756,8 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
     }
     CK(cudaMemset(s.buf[c], 0, colour_bytes));
     s.plane0[c] = s.buf[c] + ctx->ps;
-    CK(cudaMalloc(&s.partials[c], (size_t)ctx->grid_cap * NTERMS * sizeof(double)));
+    // up to 3 launches (interior + 2 boundary planes) per pass write partials
+    CK(cudaMalloc(&s.partials[c], (size_t)4 * ctx->grid_cap * NTERMS * sizeof(double)));
   }
   if (ctx->d == 3) {
     int r = make_tensor_maps(ctx, s);
@@ -726,6 +770,9 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
   s.stage_planes = (int)std::max<size_t>(1, std::min<size_t>(s.nx, (256u << 20) / nat_plane));
   CK(cudaMalloc(&s.stage, s.stage_planes * nat_plane));
   CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s.cstream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&s.ev_bnd, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s.ev_xch, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
   CK(cudaEventCreate(&s.ev_t0));
   CK(cudaEventCreate(&s.ev_t1));
@@ -896,6 +943,10 @@ int kgs_destroy(kgs_ctx* ctx) {
     if (s.ev_done) cudaEventDestroy(s.ev_done);
     if (s.ev_t0) cudaEventDestroy(s.ev_t0);
     if (s.ev_t1) cudaEventDestroy(s.ev_t1);
+    if (s.cstream) cudaStreamSynchronize(s.cstream);
+    if (s.ev_bnd) cudaEventDestroy(s.ev_bnd);
+    if (s.ev_xch) cudaEventDestroy(s.ev_xch);
+    if (s.cstream) cudaStreamDestroy(s.cstream);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   delete ctx;
@@ -1087,6 +1138,8 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
   if (r) return r;
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
+    // the step ends when the last halo exchange has landed
+    if (s.xch_pending) CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
     CK(cudaEventRecord(s.ev_t1, s.stream));
   }
   r = sync_all(ctx);
