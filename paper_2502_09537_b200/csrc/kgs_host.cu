@@ -73,8 +73,12 @@ struct Slab {
   double* plane0[2] = {nullptr, nullptr}; // colour c, element (x=0,f=0,y=0,k=0)
   MarchMaps maps[6][2];  // [march variant][colour]: TMA descriptors
   bool has_tmaps[6] = {};  // variant fits this geometry
-  int* prog = nullptr;     // fused sweep: K3 progress per column
-  int64_t prog_cap = 0;
+  // fused steps (ping-pong): the other buffer set and its descriptors
+  double* alt[2] = {nullptr, nullptr};
+  double* alt0[2] = {nullptr, nullptr};
+  MarchMaps amaps[6][2];
+  StepMaps smap[2];        // red of [0] the current set, [1] the other set
+  bool has_smap = false;
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
   double* records = nullptr;                 // device [cap * NTERMS]
@@ -119,8 +123,9 @@ struct kgs_ctx {
   // pending and fuses with the next call's head when the coefficients match
   bool pending = false;
   Coeffs pend_c{};
-  int tune_sweep = 0;      // fused one-sweep DP-AVF2 steps (experimental, opt-in)
-  int tune_sweep_dbg = 0;  // timing experiments only (results invalid)
+  int tune_fused = 0;      // fused one-march DP-AVF2 steps (opt-in until faster)
+  int tune_fused_xc = 128; // fused step: K4 planes per unit
+  bool alt_failed = false; // the second buffer set did not fit: two-pass steps
   int64_t timed_pts = 0;   // points updated twice per timed launch
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;
@@ -171,6 +176,7 @@ int pow2ceil(int v) {
 PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   PassGeom g{};
   g.own = s.plane0[col];
+  g.own_out = g.own;
   g.oth = s.plane0[col ^ 1];
   g.ps = ctx->ps;
   g.pp = ctx->pp;
@@ -278,7 +284,7 @@ CUtensorMapL2promotion promo(int v) {
 // 4-D view of one colour array with dims ordered (slot, field, row, plane)
 // -- strides 8, pp*8, nk*8, ps*8 bytes -- so that a box lands in shared
 // memory as [row][field][slot] (MarchSmem); per variant four box shapes.
-int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
+int make_maps_for(kgs_ctx* ctx, Slab& s, double* const bufs[2], MarchMaps (&maps)[6][2]) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {(cuuint64_t)ctx->nk, 4, (cuuint64_t)ctx->ny,
@@ -296,11 +302,11 @@ int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
     const cuuint32_t col[4] = {2, 3, (cuuint32_t)ty, 1};
     const cuuint32_t own[4] = {(cuuint32_t)tk, 4, (cuuint32_t)ty, 1};
     for (int c = 0; c < 2; ++c) {
-      MarchMaps& m = s.maps[v][c];
+      MarchMaps& m = maps[v][c];
       CUtensorMap* outs[4] = {&m.centre, &m.row, &m.col, &m.own};
       const cuuint32_t* boxes[4] = {centre, row, col, own};
       for (int i = 0; i < 4; ++i) {
-        CUresult r = enc(outs[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf[c], dims, strides,
+        CUresult r = enc(outs[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[c], dims, strides,
                          boxes[i], es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          promo(i == 3 ? ctx->tune_promo_tile : ctx->tune_promo_halo),
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -311,6 +317,46 @@ int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
     }
   }
   return KGS_OK;
+}
+
+// fused step: red pieces of one buffer set (StepSmem layout)
+constexpr int kStepTY = 16, kStepTK = 32;
+using StepS = StepSmem<kStepTY, kStepTK>;
+
+int make_step_maps(kgs_ctx* ctx, const Slab& s, double* red, StepMaps& m) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)ctx->nk, 4, (cuuint64_t)ctx->ny,
+                              (cuuint64_t)(s.nx + 2)};
+  const cuuint64_t strides[3] = {(cuuint64_t)ctx->pp * 8, (cuuint64_t)ctx->rs * 8,
+                                 (cuuint64_t)ctx->ps * 8};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const cuuint32_t centre[4] = {kStepTK, 3, kStepTY, 1};
+  const cuuint32_t rows2[4] = {kStepTK, 3, 2, 1};
+  const cuuint32_t col[4] = {2, 3, kStepTY, 1};
+  const cuuint32_t corner[4] = {2, 3, 1, 1};
+  CUtensorMap* outs[4] = {&m.centre, &m.rows2, &m.col, &m.corner};
+  const cuuint32_t* boxes[4] = {centre, rows2, col, corner};
+  for (int i = 0; i < 4; ++i) {
+    CUresult r = enc(outs[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, red, dims, strides, boxes[i],
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     promo(ctx->tune_promo_halo), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled(step box %d) failed: %d", i, (int)r);
+  }
+  return KGS_OK;
+}
+
+int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
+  int r = make_maps_for(ctx, s, s.buf, s.maps);
+  if (!r && s.alt[0]) r = make_maps_for(ctx, s, s.alt, s.amaps);
+  s.has_smap = false;
+  if (!r && s.alt[0] && ctx->ny % kStepTY == 0 && ctx->nk % kStepTK == 0) {
+    r = make_step_maps(ctx, s, s.buf[1], s.smap[0]);
+    if (!r) r = make_step_maps(ctx, s, s.alt[1], s.smap[1]);
+    if (!r) s.has_smap = true;
+  }
+  return r;
 }
 
 template <typename Var, int COL, int OP1, int OP2, bool DIAG, bool CHECK, int DBG = 0>
@@ -383,63 +429,152 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   return KGS_OK;
 }
 
-// ---- fused step sweep (variant 0 tiles) ----------------------------------
-constexpr size_t kSweepSmem = SweepSmem<MV0::TY, MV0::TK>::bytes;
+// ---- fused steps (ping-pong buffer sets) ---------------------------------
+bool needs_exchange(const kgs_ctx* ctx);
+int exchange(kgs_ctx* ctx, int col);
 
-bool sweep_eligible(const kgs_ctx* ctx, const Slab& s) {
-  return ctx->tune_sweep && ctx->tune_xc >= 0 && ctx->d == 3 && ctx->slabs.size() == 1 &&
-         !(ctx->dist && ctx->nranks > 1) && s.has_tmaps[0] && s.nx >= 4;
+// Geometry-only test (no allocation): 3-D, tiles divide the planes, and a
+// multi-slab run leaves interior K4 planes [1, nx-1).
+bool fused_geometry(const kgs_ctx* ctx) {
+  if (!ctx->tune_fused || ctx->alt_failed || ctx->d != 3 || ctx->tune_xc < 0) return false;
+  if (ctx->ny % kStepTY || ctx->nk % kStepTK) return false;
+  for (auto& s : ctx->slabs)
+    if (s.nx < 4) return false;
+  return true;
+}
+
+// Allocate the second buffer set on first use; if it does not fit, run
+// two-pass steps from then on (same results, more traffic).
+bool fused_ready(kgs_ctx* ctx) {
+  if (!fused_geometry(ctx)) return false;
+  for (auto& s : ctx->slabs) {
+    if (s.alt[0] && s.has_smap) continue;
+    if (cudaSetDevice(s.dev) != cudaSuccess) return false;
+    const size_t colour_bytes = (size_t)(s.nx + 2) * ctx->ps * sizeof(double);
+    for (int c = 0; c < 2 && !ctx->alt_failed; ++c) {
+      if (s.alt[c]) continue;
+      if (cudaMalloc(&s.alt[c], colour_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        s.alt[c] = nullptr;
+        ctx->alt_failed = true;
+      } else {
+        s.alt0[c] = s.alt[c] + ctx->ps;
+      }
+    }
+    if (ctx->alt_failed || make_tensor_maps(ctx, s) || !s.has_smap) {
+      for (auto& t : ctx->slabs)
+        for (int c = 0; c < 2; ++c) {
+          if (t.alt[c]) cudaFree(t.alt[c]);
+          t.alt[c] = t.alt0[c] = nullptr;
+        }
+      ctx->alt_failed = true;
+      return false;
+    }
+  }
+  return true;
+}
+
+void swap_sets(kgs_ctx* ctx) {
+  for (auto& s : ctx->slabs) {
+    for (int c = 0; c < 2; ++c) {
+      std::swap(s.buf[c], s.alt[c]);
+      std::swap(s.plane0[c], s.alt0[c]);
+    }
+    std::swap(s.maps, s.amaps);
+    std::swap(s.smap[0], s.smap[1]);
+  }
 }
 
 template <bool DIAG, int K4OP2>
-int launch_sweep(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no) {
-  constexpr int MINB = DIAG ? 1 : 2;
-  auto kern = sweep_pass<DIAG, K4OP2, MV0::TY, MV0::TK, MINB>;
+int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int xb) {
+  constexpr int NT = kStepTY * kStepTK;
+  auto kern = step_pass<DIAG, K4OP2, kStepTY, kStepTK, 2>;
   static int occ = 0;
   if (occ == 0) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MV0::NT, kSweepSmem));
-    if (occ < 1) return fail(ctx, KGS_ECUDA, "sweep kernel does not fit on an SM");
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)StepS::bytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, StepS::bytes));
+    if (occ < 1) return fail(ctx, KGS_ECUDA, "fused step kernel does not fit on an SM");
   }
-  const int nkt = ctx->nk / MV0::TK, nyt = ctx->ny / MV0::TY;
-  SweepCfg sc;
-  sc.ncols = nkt * nyt;
-  sc.D = 3 * nkt;
-  sc.nunits = (int64_t)sc.ncols + sc.D;
-  sc.dbg = ctx->tune_sweep_dbg;
-  if (s.prog_cap < sc.ncols) {
-    if (s.prog) CK(cudaFree(s.prog));
-    s.prog = nullptr;
-    CK(cudaMalloc(&s.prog, (size_t)sc.ncols * sizeof(int)));
-    s.prog_cap = sc.ncols;
-  }
-  CK(cudaMemsetAsync(s.prog, 0, (size_t)sc.ncols * sizeof(int), s.stream));
-  // persistent grid no larger than the co-resident capacity: the progress
-  // waits point only to earlier units, which is deadlock-free only if every
-  // launched block is resident
-  const int64_t grid = std::min<int64_t>({sc.nunits, (int64_t)occ * ctx->nsm, ctx->grid_cap});
-  PassGeom gb = make_geom(ctx, s, 0, 0, s.nx), gr = make_geom(ctx, s, 1, 0, s.nx);
-  kern<<<(unsigned)grid, MV0::NT, kSweepSmem, s.stream>>>(
-      s.maps[0][1], s.maps[0][0], gb, gr, c, s.partials[0], s.partials[1], s.bad, step_no,
-      s.prog, sc);
+  StepGeom g{};
+  g.rold = s.plane0[1];
+  g.bold = s.plane0[0];
+  g.rnew = s.alt0[1];
+  g.bnew = s.alt0[0];
+  g.ps = ctx->ps;
+  g.pp = ctx->pp;
+  g.rs = ctx->rs;
+  g.nx = s.nx;
+  g.ny = ctx->ny;
+  g.nk = ctx->nk;
+  g.x0 = s.x0;
+  g.wrap = needs_exchange(ctx) ? 0 : 1;
+  g.xa = xa;
+  g.xb = xb;
+  g.wa = 0;
+  g.wb = s.nx;
+  g.xc = std::max(1, std::min(ctx->tune_fused_xc, xb - xa));
+  const int64_t ncols = (int64_t)(ctx->ny / kStepTY) * (ctx->nk / kStepTK);
+  g.nunits = (int64_t)((xb - xa + g.xc - 1) / g.xc) * ncols;
+  const int64_t grid = std::min<int64_t>({g.nunits, (int64_t)occ * ctx->nsm, ctx->grid_cap});
+  kern<<<(unsigned)grid, NT, StepS::bytes, s.stream>>>(
+      s.smap[0], g, c, s.partials[1] + (int64_t)s.npart[1] * NTERMS, s.bad, step_no);
   ctx->launches++;
-  if (DIAG) { s.npart[0] = (int)grid; s.npart[1] = (int)grid; }
+  if (DIAG) s.npart[1] += (int)grid;
   CK(cudaGetLastError());
   return KGS_OK;
 }
 
-int sweep_step(kgs_ctx* ctx, bool diag, bool last, const Coeffs& c, int step_no) {
-  Slab& s = ctx->slabs[0];
-  CK(cudaSetDevice(s.dev));
-  if (diag) return last ? launch_sweep<true, OP_NONE>(ctx, s, c, step_no)
-                        : launch_sweep<true, OP_BASE>(ctx, s, c, step_no);
-  return last ? launch_sweep<false, OP_NONE>(ctx, s, c, step_no)
-              : launch_sweep<false, OP_BASE>(ctx, s, c, step_no);
+int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
+                bool check, const Coeffs& c, int step_no, int xa, int xb,
+                const double* own_in);
+
+// One DP-AVF2 step n as a fused march (K3(n) then K4(n), or the red adjoint
+// tail when `last`), step-n state in the current set, result in the other;
+// the sets are swapped after the launch.  Several slabs: the march does K4
+// on planes [1, nx-1) only; the black faces are exchanged and K4 on planes
+// 0 and nx-1 runs as a small pass reading the old red (own_in) and the new
+// black ghosts, writing the new red; then the red faces are exchanged.
+int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) {
+  const bool multi = needs_exchange(ctx);
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    if (s.xch_pending) {   // red ghosts of the current set (K3 at planes 0, nx-1)
+      CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+      s.xch_pending = false;
+    }
+    if (rec) { s.npart[1] = 0; s.npart[0] = 0; }
+    const int xa = multi ? 1 : 0, xb = multi ? s.nx - 1 : s.nx;
+    int r;
+    if (rec) r = last ? launch_step<true, OP_NONE>(ctx, s, c, step_no, xa, xb)
+                      : launch_step<true, OP_BASE>(ctx, s, c, step_no, xa, xb);
+    else     r = last ? launch_step<false, OP_NONE>(ctx, s, c, step_no, xa, xb)
+                      : launch_step<false, OP_BASE>(ctx, s, c, step_no, xa, xb);
+    if (r) return r;
+  }
+  swap_sets(ctx);
+  if (!multi) return KGS_OK;
+  int r = exchange(ctx, 0);
+  const int op2 = last ? OP_NONE : OP_BASE;
+  for (auto& s : ctx->slabs) {
+    if (r) return r;
+    CK(cudaSetDevice(s.dev));
+    if (s.xch_pending) {
+      CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+      s.xch_pending = false;
+    }
+    r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, 0, 1, s.alt0[1]);
+    if (!r) r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, s.nx - 1, s.nx,
+                            s.alt0[1]);
+  }
+  if (!r) r = exchange(ctx, 1);
+  return r;
 }
 
 // march variant to use for this pass, or -1 for the simple kernel
 int march_variant(const kgs_ctx* ctx, const Slab& s, const PassGeom& g) {
   if (ctx->d != 3 || ctx->tune_xc < 0 || g.xb - g.xa < 1) return -1;
+  if (g.own != g.own_out) return -1;  // reads another buffer: simple kernel
   int v = ctx->tune_variant;
   if (v >= 0 && v < kMarchVariants && s.has_tmaps[v]) return v;
   for (v = 0; v < kMarchVariants; ++v)   // fall back to any eligible variant
@@ -493,9 +628,13 @@ int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
               op1, op2, (int)diag, (int)check);
 }
 
+// own_in: read this colour from another buffer (same geometry) and write
+// the result to the current one; uses the simple kernel.
 int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
-                bool check, const Coeffs& c, int step_no, int xa = 0, int xb = -1) {
+                bool check, const Coeffs& c, int step_no, int xa = 0, int xb = -1,
+                const double* own_in = nullptr) {
   PassGeom g = make_geom(ctx, s, col, xa, xb < 0 ? s.nx : xb);
+  if (own_in) g.own = const_cast<double*>(own_in);
   switch (ctx->d * 2 + col) {
     case 2: return launch_col<1, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
     case 3: return launch_col<1, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
@@ -939,7 +1078,8 @@ int kgs_destroy(kgs_ctx* ctx) {
     if (s.records) cudaFree(s.records);
     if (s.bad) cudaFree(s.bad);
     if (s.stage) cudaFree(s.stage);
-    if (s.prog) cudaFree(s.prog);
+    for (int c = 0; c < 2; ++c)
+      if (s.alt[c]) cudaFree(s.alt[c]);
     if (s.ev_done) cudaEventDestroy(s.ev_done);
     if (s.ev_t0) cudaEventDestroy(s.ev_t0);
     if (s.ev_t1) cudaEventDestroy(s.ev_t1);
@@ -1111,15 +1251,16 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
   const bool defer = (flags & KGS_STEP_DEFER_TAIL) &&
                      !(record_stride > 0 && last % record_stride == 0);
   int64_t slot = 0;
-  const bool sweep = sweep_eligible(ctx, ctx->slabs[0]);
+  const bool fused = fused_ready(ctx);
+  int64_t all_pts = 0;
+  for (auto& s : ctx->slabs) all_pts += (int64_t)s.nx * ctx->ny * ctx->nk * 2;
   for (int64_t i = 1; i <= nsteps && !r; ++i) {
     const int64_t n = step_offset + i;
     const bool rec = record_stride > 0 && n % record_stride == 0;
-    if (sweep && !(i == nsteps && defer)) {
-      // one fused sweep: K3(n) and K4(n) (the tail adjoint on the last step)
-      const int64_t pts = (int64_t)ctx->slabs[0].nx * ctx->ny * ctx->nk * 2;
-      r = timed(ctx, pts, [&] { return sweep_step(ctx, rec, i == nsteps, c, (int)n); });
-      if (!r && rec) r = finalize_record(ctx, slot++, true);
+    if (fused && !(i == nsteps && defer)) {
+      // one fused march: K3(n) and K4(n) (the tail adjoint on the last step)
+      r = timed(ctx, all_pts, [&] { return step_fused(ctx, rec, i == nsteps, c, (int)n); });
+      if (!r && rec) r = finalize_record(ctx, slot++, false);
       continue;
     }
     // K3: black base(n) + adjoint(n)
@@ -1324,8 +1465,8 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "march_variant") ctx->tune_variant = value;
   else if (n == "march_planes") ctx->tune_xc = value;
   else if (n == "blocks_per_sm") ctx->tune_occ = value;
-  else if (n == "fused_sweep") ctx->tune_sweep = value;
-  else if (n == "sweep_debug") ctx->tune_sweep_dbg = value;
+  else if (n == "fused_step") ctx->tune_fused = value;
+  else if (n == "fused_planes") ctx->tune_fused_xc = std::max(1, value);
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }

@@ -273,20 +273,28 @@ def test_step_at_a_time_with_deferred_tail_is_bitwise(golden):
     dev.close()
 
 
-@pytest.mark.parametrize("N,steps,stride", [(128, 7, 3), (256, 4, 4), (128, 1, 1)])
-def test_fused_sweep_matches_two_pass_and_oracle(N, steps, stride):
-    """One fused sweep per step (K3 + lagged K4 with progress flags) gives the
-    same bits as two colour passes, the same energy records, and (128^3) the
-    same bits as the C oracle of the reference algorithm."""
+@pytest.mark.parametrize("N,steps,stride,slabs,planes", [
+    (128, 7, 3, 1, 0), (256, 4, 4, 1, 0), (128, 1, 1, 1, 0), (64, 3, 1, 1, 0),
+    (192, 3, 3, 1, 50), (128, 5, 5, 2, 0), (128, 4, 2, 4, 7), (64, 2, 1, 8, 0)])
+def test_fused_step_matches_two_pass_and_oracle(N, steps, stride, slabs, planes):
+    """One fused march per step (K3 on the tile + ring, K4 one plane behind,
+    ping-pong buffer sets) gives the same bits as two colour passes, energy
+    records equal to summation order, and (N <= 128) the same bits as the C
+    oracle of the reference algorithm -- for one slab (x wraps in the
+    kernel) and for several slabs (K4 boundary planes after the black face
+    exchange), with chunk sizes that do not divide the slab."""
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(N)
     s0 = sc.state(g) if N <= 128 else None
     args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    ex = None if slabs == 1 else kgs.CudaExecutor((0,), slabs_per_device=slabs)
     outs = []
     for fused in (0, 1):
-        dev = (kgs.DeviceFieldState.from_host(s0, g) if s0 is not None
-               else kgs.DeviceFieldState.from_preset("ellipsoids3d", g))
-        dev.ctx.set_param("fused_sweep", fused)
+        dev = (kgs.DeviceFieldState.from_host(s0, g, ex) if s0 is not None
+               else kgs.DeviceFieldState.from_preset("ellipsoids3d", g, ex))
+        dev.ctx.set_param("fused_step", fused)
+        if planes:
+            dev.ctx.set_param("fused_planes", planes)
         terms, bad = dev.ctx.step_dpavf2(args, steps, 0, stride)
         assert bad == 0
         outs.append((dev.to_host(), terms))
@@ -300,21 +308,32 @@ def test_fused_sweep_matches_two_pass_and_oracle(N, steps, stride):
         assert_bitwise(outs[1][0], ref)
 
 
-def test_fused_sweep_deferred_tail_and_nonfinite():
+@pytest.mark.parametrize("slabs", [1, 2])
+def test_fused_step_deferred_tail_and_nonfinite(slabs):
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(128)
     s0 = sc.state(g)
     coeffs = kgs.precompute_coefficients(sc.params, 0.005, g)
     sch = kgs.checkerboard_schedule(g)
-    dev = kgs.DeviceFieldState.from_host(s0, g)
+    ex = None if slabs == 1 else kgs.CudaExecutor((0,), slabs_per_device=slabs)
+    dev = kgs.DeviceFieldState.from_host(s0, g, ex)
     ref = s0.copy()
     for _ in range(3):
-        kgs.step_dpavf2(dev, sch, coeffs, None, g)
-    oracle.CheckerboardOracle(3, 128).step_dpavf2(ref, coeffs.kernel_args(), 3, workers=8)
+        kgs.step_dpavf2(dev, sch, coeffs, ex, g)
+    dev.ctx.step_dpavf2(coeffs.kernel_args(), 4, 3, 0)
+    oracle.CheckerboardOracle(3, 128).step_dpavf2(ref, coeffs.kernel_args(), 7, workers=8)
     assert_bitwise(dev.to_host(), ref)
     bad = s0.copy()
     bad.U[12345] = np.inf
     dev.upload(bad)
     _, first_bad = dev.ctx.step_dpavf2(coeffs.kernel_args(), 3, 0, 0)
     assert first_bad == 1
+    late = s0.copy()
+    dev.upload(late)
+    dev.ctx.step_dpavf2(coeffs.kernel_args(), 2, 0, 0)
+    st = dev.to_host()
+    st.P[777] = np.nan          # a red or black point of a middle plane
+    dev.upload(st)
+    _, first_bad = dev.ctx.step_dpavf2(coeffs.kernel_args(), 3, 2, 0)
+    assert first_bad == 3
     dev.close()

@@ -1,7 +1,9 @@
-"""Run fused-sweep steps at N^3 (for ncu / timing).  python tools/profile_sweep.py [--N 1024]"""
+"""Run a few fused DP-AVF2 steps (for ncu: -k regex:step_pass).
+
+    python tools/profile_step.py [--N 1024] [--steps 2] [--fused 1] [--planes 0]
+"""
 import argparse
 import sys
-import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -11,17 +13,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--N", type=int, default=1024)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--fused", type=int, default=1)
-ap.add_argument("--dbg", type=int, default=0)
+ap.add_argument("--planes", type=int, default=0)
 a = ap.parse_args()
 sc = kgs.get_scenario("ellipsoids3d")
 g = sc.default_grid(a.N)
 dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
-dev.ctx.set_param("fused_sweep", a.fused)
-dev.ctx.set_param("sweep_debug", a.dbg)
+dev.ctx.set_param("fused_step", a.fused)
+if a.planes:
+    dev.ctx.set_param("fused_planes", a.planes)
 args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
-dev.ctx.step_dpavf2(args, 1)
-dev.ctx.pass_timing(True)
-t = time.perf_counter()
-dev.ctx.step_dpavf2(args, a.steps)
-n, ms, pts = dev.ctx.pass_stats()
-print(f"N={a.N} fused={a.fused} dbg={a.dbg}: {ms / n:.3f} ms per timed launch ({n} launches, {pts} pts)")
+dev.ctx.step_dpavf2(args, a.steps, 0, 0)
+print(f"N={a.N} steps={a.steps}: {dev.ctx.last_step_ms() / a.steps:.3f} ms/step")
