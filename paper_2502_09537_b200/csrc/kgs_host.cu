@@ -125,6 +125,7 @@ struct kgs_ctx {
   Coeffs pend_c{};
   int tune_fused = 0;      // fused one-march DP-AVF2 steps (opt-in until faster)
   int tune_fused_xc = 128; // fused step: K4 planes per unit
+  int tune_fused_dbg = 0;  // fused step timing experiments (results invalid)
   bool alt_failed = false; // the second buffer set did not fit: two-pass steps
   int64_t timed_pts = 0;   // points updated twice per timed launch
   // per-pass timing (slab 0's stream): event pairs around fused passes
@@ -514,6 +515,7 @@ int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int
   g.wa = 0;
   g.wb = s.nx;
   g.xc = std::max(1, std::min(ctx->tune_fused_xc, xb - xa));
+  g.dbg = ctx->tune_fused_dbg;
   const int64_t ncols = (int64_t)(ctx->ny / kStepTY) * (ctx->nk / kStepTK);
   g.nunits = (int64_t)((xb - xa + g.xc - 1) / g.xc) * ncols;
   const int64_t grid = std::min<int64_t>({g.nunits, (int64_t)occ * ctx->nsm, ctx->grid_cap});
@@ -1467,6 +1469,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "blocks_per_sm") ctx->tune_occ = value;
   else if (n == "fused_step") ctx->tune_fused = value;
   else if (n == "fused_planes") ctx->tune_fused_xc = std::max(1, value);
+  else if (n == "fused_debug") ctx->tune_fused_dbg = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }

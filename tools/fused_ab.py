@@ -8,7 +8,7 @@ import sys
 import paper_2502_09537_b200 as kgs
 
 
-def run(N, steps, fused, planes=0, slabs=1):
+def run(N, steps, fused, planes=0, slabs=1, dbg=0):
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(N)
     ex = None if slabs == 1 else kgs.CudaExecutor((0,), slabs_per_device=slabs)
@@ -17,6 +17,8 @@ def run(N, steps, fused, planes=0, slabs=1):
     ctx.set_param("fused_step", fused)
     if planes:
         ctx.set_param("fused_planes", planes)
+    if dbg:
+        ctx.set_param("fused_debug", dbg)
     args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
     ctx.step_dpavf2(args, 3, 0, 0)
     launches0 = ctx.launch_count() if hasattr(ctx, "launch_count") else None
@@ -34,6 +36,8 @@ def main():
     for p in planes:
         out[f"fused_xc{p or 128}"] = run(N, steps, 1, p)
     out["fused_4slabs"] = run(N, steps, 1, 0, 4)
+    for dbg in (1, 2, 4, 7):   # timing only: 1 no ring, 2 no K4 math, 4 no K3 math
+        out[f"fused_dbg{dbg}"] = run(N, steps, 1, 0, 1, dbg)
     print(json.dumps({"N": N, **out}))
 
 
