@@ -185,10 +185,13 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
 
 /* Named tuning knob (results never depend on it): "march_variant",
  * "march_planes", "march_sync" (planes between cluster barriers of the
- * clustered variants), "blocks_per_sm", "fused_sweep" (1: one fused sweep
- * per DP-AVF2 step when the geometry allows -- experimental, bitwise equal
- * but currently slower; 0, the default: two colour passes).
- * KGS_EINVAL for unknown names. */
+ * clustered variants), "blocks_per_sm", "fused_step" (1: one fused march
+ * per DP-AVF2 step -- K3 and K4 with ping-pong buffer sets, allocated on
+ * first use; 3-D, rows % 16 == 0, slots % 32 == 0 -- bitwise equal but
+ * currently slower; 0, the default: two colour passes), "fused_planes"
+ * (fused step: K4 planes per work unit, default 128), "fused_debug"
+ * (timing experiments only, CORRUPTS results: 1 no ring K3, 2 no K4
+ * arithmetic, 4 no K3 arithmetic).  KGS_EINVAL for unknown names. */
 int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 
 /* L2 sector promotion of the marching kernel's TMA boxes (0 none, 1 64 B,
