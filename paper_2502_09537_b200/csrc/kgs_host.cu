@@ -126,6 +126,7 @@ struct kgs_ctx {
   int tune_fused = 0;      // fused one-march DP-AVF2 steps (opt-in until faster)
   int tune_fused_xc = 128; // fused step: K4 planes per unit
   int tune_fused_dbg = 0;  // fused step timing experiments (results invalid)
+  int tune_resident = 1;   // small grids: whole call in one launch (shared memory)
   bool alt_failed = false; // the second buffer set did not fit: two-pass steps
   int64_t timed_pts = 0;   // points updated twice per timed launch
   // per-pass timing (slab 0's stream): event pairs around fused passes
@@ -428,6 +429,50 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   if (DIAG) s.npart[COL] += (int)grid;
   CK(cudaGetLastError());
   return KGS_OK;
+}
+
+// ---- resident steps (whole state in one CTA's shared memory) -------------
+constexpr size_t kResidentMaxBytes = 200 * 1024;
+
+bool resident_eligible(const kgs_ctx* ctx) {
+  if (!ctx->tune_resident || ctx->slabs.size() != 1 || (ctx->dist && ctx->nranks > 1))
+    return false;
+  const Slab& s = ctx->slabs[0];
+  return (size_t)s.nx * ctx->ps * 2 * sizeof(double) <= kResidentMaxBytes;
+}
+
+template <int D>
+int launch_resident_d(kgs_ctx* ctx, Slab& s, const Coeffs& c, const ResidentCfg& rc) {
+  auto kern = resident_steps<D>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kResidentMaxBytes));
+    attr = true;
+  }
+  PassGeom gb = make_geom(ctx, s, 0, 0, s.nx), gr = make_geom(ctx, s, 1, 0, s.nx);
+  const size_t bytes = (size_t)s.nx * ctx->ps * 2 * sizeof(double);
+  kern<<<1, 1024, bytes, s.stream>>>(gb, gr, c, rc, s.records, s.bad);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+int launch_resident(kgs_ctx* ctx, const Coeffs& c, int64_t nsteps, int64_t step_offset,
+                    int64_t record_stride, bool head_fused, bool defer) {
+  Slab& s = ctx->slabs[0];
+  CK(cudaSetDevice(s.dev));
+  ResidentCfg rc;
+  rc.nsteps = nsteps;
+  rc.step_offset = step_offset;
+  rc.record_stride = record_stride;
+  rc.head_fused = head_fused ? 1 : 0;
+  rc.defer = defer ? 1 : 0;
+  switch (ctx->d) {
+    case 1: return launch_resident_d<1>(ctx, s, c, rc);
+    case 2: return launch_resident_d<2>(ctx, s, c, rc);
+    default: return launch_resident_d<3>(ctx, s, c, rc);
+  }
 }
 
 // ---- fused steps (ping-pong buffer sets) ---------------------------------
@@ -1239,19 +1284,30 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
     CK(cudaSetDevice(s.dev));
     CK(cudaEventRecord(s.ev_t0, s.stream));
   }
-  // head: base red(first step) -- fused with a deferred red adjoint of the
-  // previous call when its coefficients are the same (bitwise neutral)
-  if (ctx->pending && std::memcmp(&ctx->pend_c, &c, sizeof c) == 0) {
-    ctx->pending = false;
-    r = all_passes(ctx, 1, OP_ADJ, OP_BASE, false, false, c, 0);
-  } else {
-    r = flush_pending(ctx);
-    if (!r) r = all_passes(ctx, 1, OP_BASE, OP_NONE, false, false, c, 0);
-  }
-  if (!r) r = exchange(ctx, 1);
   const int64_t last = step_offset + nsteps;
   const bool defer = (flags & KGS_STEP_DEFER_TAIL) &&
                      !(record_stride > 0 && last % record_stride == 0);
+  const bool resident = resident_eligible(ctx);
+  // head: base red(first step) -- fused with a deferred red adjoint of the
+  // previous call when its coefficients are the same (bitwise neutral)
+  const bool head_fused = ctx->pending && std::memcmp(&ctx->pend_c, &c, sizeof c) == 0;
+  if (head_fused) {
+    ctx->pending = false;
+    if (!resident) r = all_passes(ctx, 1, OP_ADJ, OP_BASE, false, false, c, 0);
+  } else {
+    r = flush_pending(ctx);
+    if (!r && !resident) r = all_passes(ctx, 1, OP_BASE, OP_NONE, false, false, c, 0);
+  }
+  if (!r && resident) {
+    // the whole call in one launch (state in shared memory)
+    r = launch_resident(ctx, c, nsteps, step_offset, record_stride, head_fused, defer);
+    if (!r && defer) {
+      ctx->pending = true;
+      ctx->pend_c = c;
+    }
+    nsteps = 0;   // skip the per-step loop below
+  }
+  if (!r && !resident) r = exchange(ctx, 1);
   int64_t slot = 0;
   const bool fused = fused_ready(ctx);
   int64_t all_pts = 0;
@@ -1470,6 +1526,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "fused_step") ctx->tune_fused = value;
   else if (n == "fused_planes") ctx->tune_fused_xc = std::max(1, value);
   else if (n == "fused_debug") ctx->tune_fused_dbg = value;
+  else if (n == "resident") ctx->tune_resident = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }

@@ -337,3 +337,35 @@ def test_fused_step_deferred_tail_and_nonfinite(slabs):
     _, first_bad = dev.ctx.step_dpavf2(coeffs.kernel_args(), 3, 2, 0)
     assert first_bad == 3
     dev.close()
+
+
+@pytest.mark.parametrize("name", run_names())
+def test_resident_kernel_matches_passes_and_reference(golden, name):
+    """Small grids run a whole call in ONE launch with the state in shared
+    memory; the fields are bitwise the per-pass path's (and the reference's),
+    records equal to reduction order, for every golden run (records every
+    step, a deferred tail, and a mid-call non-finite value)."""
+    c = golden.case(name)
+    args = c.kernel_args
+    n = c.meta["n_steps"]
+    outs = []
+    for resident in (0, 1):
+        dev = kgs.DeviceFieldState.from_host(c.state(0), c.grid)
+        dev.ctx.set_param("resident", resident)
+        terms, bad = dev.ctx.step_dpavf2(args, n, 0, 1)
+        assert bad == 0
+        dev.ctx.step_dpavf2(args, 2, n, 0, defer_tail=True)
+        dev.ctx.step_dpavf2(args, 1, n + 2, 1)
+        outs.append((dev.to_host(), terms))
+        st = outs[-1][0].copy()
+        st.V[st.V.size // 3] = np.nan
+        dev.upload(st)
+        _, first_bad = dev.ctx.step_dpavf2(args, 3, 10, 0)
+        assert first_bad == 11
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-13, atol=1e-300)
+    ref = c.state(0)
+    for _ in range(n + 3):
+        oracle.numpy_step_dpavf2(ref, args, c.grid)
+    assert_bitwise(outs[1][0], ref)
