@@ -201,8 +201,6 @@ def integrate(state, grid: GridSpec, params: PhysParams,
                 trace.rel_error.append(re)
                 trace.mass.append(m)
         state.t = t
-        if isinstance(state, DeviceFieldState):
-            pass
         n = n1
         if snap and n % snap == 0:
             if host is not None:

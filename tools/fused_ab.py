@@ -21,7 +21,6 @@ def run(N, steps, fused, planes=0, slabs=1, dbg=0):
         ctx.set_param("fused_debug", dbg)
     args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
     ctx.step_dpavf2(args, 3, 0, 0)
-    launches0 = ctx.launch_count() if hasattr(ctx, "launch_count") else None
     ctx.step_dpavf2(args, steps, 3, 0)
     ms = ctx.last_step_ms() / steps
     dev.close()
