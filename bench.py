@@ -293,7 +293,9 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
-        "scaling": "strong" if (args.scaling == "strong" or N == args.N) else "weak",
+        # weak: per-GPU work fixed (N = 1024 * cbrt(G) for cube G, incl. G = 1)
+        "scaling": "weak" if (args.scaling == "weak" and round(world ** (1 / 3)) ** 3 == world)
+                   else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"3D KGS {SCENARIO} N={N}^3 fp64, tau={TAU}, checkerboard DP-AVF2",
                    "grid_points": g.M, "updates_per_step": 2 * g.M,
