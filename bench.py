@@ -248,12 +248,18 @@ def run_ours(args):
         traffic = nc.get("dram_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-            "peak_source": pk["source"], "kernel": "colour_pass (fused K3/K4)",
+            "peak_source": pk["source"],
+            "kernel": "march_pass (fused K3/K4 colour pass, TMA ring)",
             "algorithmic_bytes_per_update": BYTES_PER_UPDATE,
             "avg_launch_ms": avg_pass_ms, "launches_timed": n_pass,
             "design_bytes_per_update": DESIGN_BYTES_PER_UPDATE,
             "design_frac": DESIGN_BYTES_PER_UPDATE * upd_per_launch / (avg_pass_ms / 1e3) / 1e9
             / pk["hbm_gbs"]}
+    if traffic:
+        # what the kernel actually moves: ncu DRAM bytes per launch / live launch time
+        roof["dram_achieved"] = traffic / (avg_pass_ms / 1e3) / 1e9
+        roof["dram_frac"] = roof["dram_achieved"] / pk["hbm_gbs"]
+        roof["dram_bytes_per_update"] = traffic / upd_per_launch
 
     # energy sanity (the timed run recorded step W+K)
     e = kgs.grid.energy_from_terms(terms[0], sc.params, g)[0] if len(terms) else None
