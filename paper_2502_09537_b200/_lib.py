@@ -125,6 +125,8 @@ def check(rc: int, ctx=None) -> None:
         raise ValueError(msg)
     if rc == KGS_ENONFINITE:
         raise FloatingPointError(msg)
+    if rc == KGS_ENOMEM:
+        raise MemoryError(msg)
     raise KgsError(rc, msg)
 
 

@@ -369,3 +369,16 @@ def test_resident_kernel_matches_passes_and_reference(golden, name):
     for _ in range(n + 3):
         oracle.numpy_step_dpavf2(ref, args, c.grid)
     assert_bitwise(outs[1][0], ref)
+
+
+def test_oversized_grid_fails_cleanly_and_device_stays_usable():
+    """2048^3 (275 GB) does not fit one B200: MemoryError naming the
+    allocation, nothing leaked -- a normal context works right after."""
+    g = kgs.GridSpec(3, -10.0, 10.0, 2048)
+    with pytest.raises(MemoryError, match="cudaMalloc"):
+        kgs.DeviceFieldState(g)
+    sc = kgs.get_scenario("ellipsoids3d")
+    g2 = sc.default_grid(64)
+    dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g2)
+    assert dev.is_finite()
+    dev.close()
