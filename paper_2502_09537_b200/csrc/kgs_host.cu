@@ -92,6 +92,7 @@ struct Slab {
   cudaEvent_t ev_bnd = nullptr;     // boundary planes of the last pass written
   cudaEvent_t ev_xch = nullptr;     // last exchange into this slab's ghosts done
   bool xch_pending = false;
+  cudaEvent_t ev_face[2] = {nullptr, nullptr};  // boundary planes of pass k written (k & 1)
 };
 
 }  // namespace
@@ -127,6 +128,12 @@ struct kgs_ctx {
   int tune_fused_xc = 128; // fused step: K4 planes per unit
   int tune_fused_dbg = 0;  // fused step timing experiments (results invalid)
   int tune_resident = 1;   // small grids: whole call in one launch (shared memory)
+  // fused halo exchange (single-process slabs): boundary launches
+  // store their faces straight into the neighbours' ghost planes
+  bool mirror = false;       // possible for this context (peer-accessible neighbours)
+  int tune_mirror = 1;       // knob "mirror_halo"
+  int64_t pass_no = 0;       // colour passes issued with the interior/boundary split
+  bool mirrored[2] = {false, false};  // faces of colour c already in the ghosts
   bool alt_failed = false; // the second buffer set did not fit: two-pass steps
   int64_t timed_pts = 0;   // points updated twice per timed launch
   // per-pass timing (slab 0's stream): event pairs around fused passes
@@ -179,6 +186,7 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   PassGeom g{};
   g.own = s.plane0[col];
   g.own_out = g.own;
+  g.mir_lo = g.mir_hi = nullptr;
   g.oth = s.plane0[col ^ 1];
   g.ps = ctx->ps;
   g.pp = ctx->pp;
@@ -574,7 +582,7 @@ int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int
 
 int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
                 bool check, const Coeffs& c, int step_no, int xa, int xb,
-                const double* own_in);
+                const double* own_in, double* mir_lo, double* mir_hi);
 
 // One DP-AVF2 step n as a fused march (K3(n) then K4(n), or the red adjoint
 // tail when `last`), step-n state in the current set, result in the other;
@@ -584,6 +592,7 @@ int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
 // black ghosts, writing the new red; then the red faces are exchanged.
 int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) {
   const bool multi = needs_exchange(ctx);
+  ctx->mirrored[0] = ctx->mirrored[1] = false;  // this path exchanges by copies
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
     if (s.xch_pending) {   // red ghosts of the current set (K3 at planes 0, nx-1)
@@ -610,9 +619,10 @@ int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) 
       CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
       s.xch_pending = false;
     }
-    r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, 0, 1, s.alt0[1]);
+    r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, 0, 1, s.alt0[1], nullptr,
+                    nullptr);
     if (!r) r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, s.nx - 1, s.nx,
-                            s.alt0[1]);
+                            s.alt0[1], nullptr, nullptr);
   }
   if (!r) r = exchange(ctx, 1);
   return r;
@@ -679,9 +689,12 @@ int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
 // the result to the current one; uses the simple kernel.
 int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
                 bool check, const Coeffs& c, int step_no, int xa = 0, int xb = -1,
-                const double* own_in = nullptr) {
+                const double* own_in = nullptr, double* mir_lo = nullptr,
+                double* mir_hi = nullptr) {
   PassGeom g = make_geom(ctx, s, col, xa, xb < 0 ? s.nx : xb);
   if (own_in) g.own = const_cast<double*>(own_in);
+  g.mir_lo = mir_lo;
+  g.mir_hi = mir_hi;
   switch (ctx->d * 2 + col) {
     case 2: return launch_col<1, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
     case 3: return launch_col<1, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
@@ -708,6 +721,10 @@ bool needs_exchange(const kgs_ctx* ctx) {
 // plane), so a face is ONE contiguous run of 3*pp doubles.
 int exchange(kgs_ctx* ctx, int col) {
   if (!needs_exchange(ctx)) return KGS_OK;  // a single slab wraps in the kernel
+  if (ctx->mirrored[col]) {  // the boundary launches already stored the faces
+    ctx->mirrored[col] = false;
+    return KGS_OK;
+  }
   const size_t face = (size_t)3 * ctx->pp;
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
@@ -780,10 +797,24 @@ int sync_all(kgs_ctx* ctx) {
 // interior planes [1, nx-1) go first -- they need no ghost data, so they
 // overlap the previous pass's halo exchange -- then the stream waits for
 // that exchange (ev_xch) and runs the two boundary planes.
+//
+// Fused halo exchange (ctx->mirror): the boundary launches of slab i also
+// store their new faces into the neighbours' ghost planes (peer pointers),
+// so no exchange follows.  Before slab i's boundary launches of pass k its
+// stream waits for both neighbours' boundary launches of pass k-1 (ev_face):
+// that is when they finished writing i's ghosts (RAW) and finished reading
+// their own ghosts that i is about to overwrite (WAR); pending copy
+// exchanges into either side are waited for as well.
 int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
                const Coeffs& c, int step_no) {
   const bool split = needs_exchange(ctx);
-  for (auto& s : ctx->slabs) {
+  const bool mirror = split && ctx->mirror && ctx->tune_mirror;
+  const bool writes = op1 != OP_NONE || op2 != OP_NONE;
+  const int64_t k = ctx->pass_no;
+  if (split) ctx->pass_no++;
+  const int ns = (int)ctx->slabs.size();
+  for (int i = 0; i < ns; ++i) {
+    Slab& s = ctx->slabs[i];
     cudaError_t e = cudaSetDevice(s.dev);
     if (e != cudaSuccess) return fail(ctx, KGS_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
     if (diag) s.npart[col] = 0;
@@ -797,11 +828,28 @@ int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
         CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
         s.xch_pending = false;
       }
-      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, 0, 1);
-      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, s.nx - 1, s.nx);
+      Slab& lo = ctx->slabs[(i - 1 + ns) % ns];
+      Slab& hi = ctx->slabs[(i + 1) % ns];
+      if (!r && mirror) {
+        CK(cudaStreamWaitEvent(s.stream, lo.ev_xch, 0));
+        CK(cudaStreamWaitEvent(s.stream, hi.ev_xch, 0));
+        if (k > 0) {
+          CK(cudaStreamWaitEvent(s.stream, lo.ev_face[(k - 1) & 1], 0));
+          CK(cudaStreamWaitEvent(s.stream, hi.ev_face[(k - 1) & 1], 0));
+        }
+      }
+      // our plane 0 is lo's ghost plane lo.nx; our plane nx-1 is hi's ghost -1
+      double* mlo = (mirror && writes) ? lo.plane0[col] + (int64_t)lo.nx * ctx->ps : nullptr;
+      double* mhi = (mirror && writes) ? hi.plane0[col] - ctx->ps : nullptr;
+      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, 0, 1, nullptr,
+                              mlo, nullptr);
+      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, s.nx - 1, s.nx,
+                              nullptr, nullptr, mhi);
+      if (!r && mirror) CK(cudaEventRecord(s.ev_face[k & 1], s.stream));
     }
     if (r) return r;
   }
+  if (mirror && writes) ctx->mirrored[col] = true;
   return KGS_OK;
 }
 
@@ -959,6 +1007,8 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
   CK(cudaStreamCreateWithFlags(&s.cstream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&s.ev_bnd, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_xch, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i)
+    CK(cudaEventCreateWithFlags(&s.ev_face[i], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
   CK(cudaEventCreate(&s.ev_t0));
   CK(cudaEventCreate(&s.ev_t1));
@@ -1047,6 +1097,18 @@ int kgs_create(int d, int64_t N, double a, double b, int nslabs,
           cudaSetDevice(s.dev);
           if (cudaDeviceEnablePeerAccess(t.dev, 0) != cudaSuccess) cudaGetLastError();
         }
+    // fused halo stores need every slab to reach its neighbours' memory
+    const int ns = (int)ctx->slabs.size();
+    ctx->mirror = ns > 1;
+    for (int i = 0; i < ns && ctx->mirror; ++i)
+      for (int dj : {-1, 1}) {
+        const int a = ctx->slabs[i].dev, b = ctx->slabs[(i + dj + ns) % ns].dev;
+        int ok = 1;
+        if (a != b && (cudaDeviceCanAccessPeer(&ok, a, b) != cudaSuccess || !ok)) {
+          cudaGetLastError();
+          ctx->mirror = false;
+        }
+      }
   }
   if (r) {
     g_last_error = ctx->err;
@@ -1133,6 +1195,8 @@ int kgs_destroy(kgs_ctx* ctx) {
     if (s.cstream) cudaStreamSynchronize(s.cstream);
     if (s.ev_bnd) cudaEventDestroy(s.ev_bnd);
     if (s.ev_xch) cudaEventDestroy(s.ev_xch);
+    for (int i = 0; i < 2; ++i)
+      if (s.ev_face[i]) cudaEventDestroy(s.ev_face[i]);
     if (s.cstream) cudaStreamDestroy(s.cstream);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
@@ -1214,6 +1278,7 @@ int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
     int r = transfer_planes(ctx, fi, x0, nx, const_cast<double*>(f[fi]), true);
     if (r) return r;
   }
+  ctx->mirrored[0] = ctx->mirrored[1] = false;  // planes written without mirroring
   int r = exchange(ctx, 0);
   if (!r) r = exchange(ctx, 1);
   if (!r) r = sync_all(ctx);
@@ -1238,6 +1303,7 @@ int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
   int r = check_range(ctx, field, x_begin, nplanes, src);
   if (!r) r = flush_pending(ctx);
   if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, const_cast<double*>(src), true);
+  ctx->mirrored[0] = ctx->mirrored[1] = false;  // planes written without mirroring
   if (!r && field < 3) r = exchange(ctx, 0);   // refresh faces (P, Q, U are halo fields)
   if (!r && field < 3) r = exchange(ctx, 1);
   if (!r) r = sync_all(ctx);
@@ -1527,6 +1593,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "fused_planes") ctx->tune_fused_xc = std::max(1, value);
   else if (n == "fused_debug") ctx->tune_fused_dbg = value;
   else if (n == "resident") ctx->tune_resident = value;
+  else if (n == "mirror_halo") ctx->tune_mirror = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }
@@ -1566,6 +1633,7 @@ int kgs_fill_preset(kgs_ctx* ctx, int preset) {
     ctx->launches++;
     CK(cudaGetLastError());
   }
+  ctx->mirrored[0] = ctx->mirrored[1] = false;  // planes written without mirroring
   int r = exchange(ctx, 0);
   if (!r) r = exchange(ctx, 1);
   if (!r) r = sync_all(ctx);

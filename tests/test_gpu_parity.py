@@ -382,3 +382,37 @@ def test_oversized_grid_fails_cleanly_and_device_stays_usable():
     dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g2)
     assert dev.is_finite()
     dev.close()
+
+
+@pytest.mark.parametrize("N,slabs", [(64, 2), (128, 4), (96, 8), (16, 2)])
+def test_fused_halo_stores_match_copy_exchange(N, slabs):
+    """Single-process slabs exchange faces by storing them from the boundary
+    launches straight into the neighbours' ghost planes (knob mirror_halo);
+    the result is bitwise the copy-based exchange's and the oracle's, with
+    records, single sweeps and step-at-a-time (deferred tail) calls mixed."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(N)
+    s0 = sc.state(g)
+    coeffs = kgs.precompute_coefficients(sc.params, 0.005, g)
+    args = coeffs.kernel_args()
+    sch = kgs.checkerboard_schedule(g)
+    ex = kgs.CudaExecutor((0,), slabs_per_device=slabs)
+    outs = []
+    for mirror in (0, 1):
+        dev = kgs.DeviceFieldState.from_host(s0, g, ex)
+        dev.ctx.set_param("mirror_halo", mirror)
+        terms, bad = dev.ctx.step_dpavf2(args, 4, 0, 2)
+        assert bad == 0
+        kgs.step_dpavf2(dev, sch, coeffs, ex, g)
+        kgs.step_dpavf2(dev, sch, coeffs, ex, g)
+        kgs.step_base(dev, sch, coeffs, ex, g)
+        kgs.step_adjoint(dev, sch, coeffs, ex, g)
+        outs.append((dev.to_host(), terms, kgs.discrete_energy(dev, sc.params, g)))
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+    ref = s0.copy()
+    orc = oracle.CheckerboardOracle(3, N)
+    orc.step_dpavf2(ref, args, 7, workers=oracle.CheckerboardOracle.max_threads())
+    assert_bitwise(outs[1][0], ref)
