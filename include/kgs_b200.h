@@ -191,7 +191,13 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
  * currently slower; 0, the default: two colour passes), "fused_planes"
  * (fused step: K4 planes per work unit, default 128), "fused_debug"
  * (timing experiments only, CORRUPTS results: 1 no ring K3, 2 no K4
- * arithmetic, 4 no K3 arithmetic).  KGS_EINVAL for unknown names. */
+ * arithmetic, 4 no K3 arithmetic), "resident" (1, the default: a grid
+ * whose state fits in one CTA's shared memory -- 32 B per point <= 200 KiB
+ * -- runs a whole kgs_step_dpavf2 call in one launch; 0: per-pass
+ * launches), "mirror_halo" (1, the default: single-process slabs store
+ * their faces from the boundary launches straight into the neighbours'
+ * ghost planes; 0: peer copies after each pass).  KGS_EINVAL for unknown
+ * names. */
 int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 
 /* L2 sector promotion of the marching kernel's TMA boxes (0 none, 1 64 B,
