@@ -1,5 +1,8 @@
 """Summarise an .ncu-rep: key throughput metrics and top stall reasons per
-kernel launch.   python tools/ncu_summary.py gpurun_out/prof.ncu-rep"""
+kernel launch.   python tools/ncu_summary.py gpurun_out/prof.ncu-rep
+With --json N POINTS SOURCE: print profiles/ncu_summary.json (the DRAM
+traffic per launch bench.py reports as roofline.traffic) for the first
+launch in the report."""
 import csv
 import io
 import subprocess
@@ -42,5 +45,30 @@ def main(path):
         print("   stalls:", ", ".join(f"{n} {100*v/tot:.0f}%" for v, n in sorted(st, reverse=True)[:8]))
 
 
+def to_json(path, N, points, source):
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, r = rows[0], rows[1], rows[2]
+
+    def val(k):
+        v = float(r[hdr.index(k)].replace(",", ""))
+        u = units[hdr.index(k)]
+        return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(u, 1.0)
+    rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+    dur = float(r[hdr.index("gpu__time_duration.sum")].replace(",", ""))
+    print(json.dumps({
+        "N": N, "world": 1, "kernel": r[hdr.index("Kernel Name")][:120],
+        "dram_bytes_per_launch": rd + wr, "dram_read_bytes_per_launch": rd,
+        "dram_write_bytes_per_launch": wr, "ncu_duration_ms": [dur],
+        "points_per_launch": points, "dram_bytes_per_update": (rd + wr) / (2 * points),
+        "source": source}, indent=1))
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    if "--json" in sys.argv:
+        i = sys.argv.index("--json")
+        to_json(sys.argv[1], int(sys.argv[i + 1]), int(sys.argv[i + 2]), sys.argv[i + 3])
+    else:
+        main(sys.argv[1])
