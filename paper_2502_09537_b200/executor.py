@@ -9,7 +9,11 @@ names the devices and the slab decomposition along axis 0:
 * ``SerialExecutor`` / ``PhasedExecutor(workers)`` -- accepted for
   drop-in compatibility; both run on one GPU (``cuda:0``).  ``workers`` is
   kept as an attribute and has no effect on the result (bitwise identical
-  for every worker count, like the reference, ``executor.py:1-8``).
+  for every worker count, like the reference, ``executor.py:1-8``).  Their
+  ``run(schedule, lane_fn)`` keeps the reference's host semantics for code
+  that drives its own lane functions (``executor.py:39-71``): the serial
+  order on the calling thread, or phase by phase over a thread pool with a
+  full barrier; the device sweeps never go through it.
 * ``CudaExecutor(devices, slabs_per_device=1)`` -- single process driving
   one or more GPUs; the grid is split into ``len(devices)*slabs_per_device``
   slabs with face halos copied between them (several slabs on one device
@@ -81,6 +85,10 @@ class SerialExecutor(_DeviceExecutor):
 
     workers = 1
 
+    def run(self, schedule, lane_fn) -> None:
+        """Host lane function over the whole serial order (executor.py:39-40)."""
+        lane_fn(schedule.serial_order())
+
 
 class PhasedExecutor(_DeviceExecutor):
     """One GPU (cuda:0); the drop-in for dpavf.executor.PhasedExecutor."""
@@ -89,6 +97,31 @@ class PhasedExecutor(_DeviceExecutor):
         if workers < 1:
             raise ValueError("workers must be >= 1")
         self.workers = workers
+        self._pool = None
+
+    def run(self, schedule, lane_fn) -> None:
+        """Host lane functions phase by phase, lanes of a parallel phase on a
+        thread pool, full barrier between phases; lane errors re-raised
+        (executor.py:60-71)."""
+        if not getattr(schedule, "validated", True):
+            raise ValueError(
+                "schedule has not passed validation; run validate_schedule first")
+        for phase in schedule.phases:
+            if phase.parallel and self.workers > 1 and len(phase.lanes) > 1:
+                if self._pool is None:
+                    from concurrent.futures import ThreadPoolExecutor
+                    self._pool = ThreadPoolExecutor(max_workers=self.workers)
+                futures = [self._pool.submit(lane_fn, lane) for lane in phase.lanes]
+                for f in futures:
+                    f.result()
+            else:
+                for lane in phase.lanes:
+                    lane_fn(lane)
+
+    def close(self) -> None:
+        if self._pool is not None:
+            self._pool.shutdown(wait=True)
+            self._pool = None
 
 
 class CudaExecutor(_DeviceExecutor):

@@ -178,3 +178,65 @@ def test_energy_from_terms_formula():
     quad = 2.0 * 4.0 + 2.0 * 8.0 + 3.0 * 12.0 + 4.0 + 0.25 * 5.0
     assert e == pytest.approx(0.25 * (0.5 * quad - 0.25 * 6.0))
     assert m == pytest.approx(0.25 * 15.0)
+
+
+class TestExecutorRun:
+    """executor.run(schedule, lane_fn) keeps the reference's host semantics
+    (dpavf/executor.py:39-71) for code that drives its own lane functions."""
+
+    def _grid(self):
+        return kgs.GridSpec(2, -1.0, 1.0, 8)
+
+    def test_serial_runs_the_serial_order_once(self):
+        g = self._grid()
+        sch = kgs.checkerboard_schedule(g, 3)
+        seen = []
+        kgs.SerialExecutor().run(sch, lambda lane: seen.append(np.array(lane)))
+        assert len(seen) == 1
+        assert np.array_equal(seen[0], sch.serial_order())
+        parity = np.indices(g.shape).sum(axis=0).ravel() % 2
+        n_red = int(parity.sum())
+        assert (parity[seen[0][:n_red]] == 1).all() and (parity[seen[0][n_red:]] == 0).all()
+
+    def test_phased_barrier_and_coverage(self):
+        import threading
+        g = self._grid()
+        sch = kgs.checkerboard_schedule(g, 4)
+        parity = np.indices(g.shape).sum(axis=0).ravel() % 2
+        log, lock = [], threading.Lock()
+
+        def lane_fn(lane):
+            with lock:
+                log.append((int(parity[lane[0]]), np.array(lane)))
+
+        with kgs.PhasedExecutor(4) as ex:
+            ex.run(sch, lane_fn)
+        colours = [c for c, _ in log]
+        assert colours == sorted(colours, reverse=True)      # every red lane before any black
+        allidx = np.sort(np.concatenate([l for _, l in log]))
+        assert np.array_equal(allidx, np.arange(g.M))          # each point exactly once
+        rev = kgs.reverse_schedule(sch)
+        log.clear()
+        with kgs.PhasedExecutor(2) as ex:
+            ex.run(rev, lane_fn)
+        assert [c for c, _ in log] == sorted(c for c, _ in log)  # black first when reversed
+
+    def test_phased_reraises_lane_errors_and_checks_validation(self):
+        g = self._grid()
+        sch = kgs.checkerboard_schedule(g, 4)
+
+        def boom(lane):
+            raise RuntimeError("lane failed")
+
+        with kgs.PhasedExecutor(4) as ex:
+            with pytest.raises(RuntimeError, match="lane failed"):
+                ex.run(sch, boom)
+        unvalidated = kgs.checkerboard_schedule(g, 2)
+        unvalidated.validated = False
+        with pytest.raises(ValueError, match="validation"):
+            kgs.PhasedExecutor(2).run(unvalidated, lambda lane: None)
+
+    def test_device_only_executors_reject_host_lanes(self):
+        g = self._grid()
+        with pytest.raises(TypeError):
+            kgs.CudaExecutor((0,)).run(kgs.checkerboard_schedule(g), lambda lane: None)
