@@ -42,17 +42,25 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+CHECKED_OUT = PKG / "libkgs_b200_checked.so"
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    """checked: -DKGS_CHECKED (index asserts that trap) into
+    libkgs_b200_checked.so, for tools/sanitize_run.py; never loaded by
+    default (select it with KGS_B200_LIB)."""
+    out = CHECKED_OUT if checked else OUT
+    if not force and not checked and up_to_date():
         return OUT
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES), "-ldl"]
+    tmp = out.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DKGS_CHECKED"] if checked else []), "-o", str(tmp),
+           *map(str, SOURCES), "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -44,7 +44,9 @@ def stub(tmp_path, monkeypatch):
         "from paper_2502_09537_b200.integrator import EnergyTrace, precompute_coefficients\n")
     (pkg / "b200.py").write_text(stub_source())
     from paper_2502_09537_b200 import _lib
-    monkeypatch.setenv("KGS_B200_LIB", str(_lib.LIB_PATH))
+    # the same file the package loaded (two copies in one process would
+    # interpose each other's symbols)
+    monkeypatch.setenv("KGS_B200_LIB", _lib.load()._name)
     monkeypatch.syspath_prepend(str(tmp_path))
     import importlib
     mod = importlib.import_module("dpavf_stub.b200")
