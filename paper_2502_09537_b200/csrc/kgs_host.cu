@@ -128,6 +128,7 @@ struct kgs_ctx {
   int tune_fused_xc = 128; // fused step: K4 planes per unit
   int tune_fused_dbg = 0;  // fused step timing experiments (results invalid)
   int tune_resident = 1;   // small grids: whole call in one launch (shared memory)
+  int tune_tstore = 2;     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
   // fused halo exchange (single-process slabs): boundary launches
   // store their faces straight into the neighbours' ghost planes
   bool mirror = false;       // possible for this context (peer-accessible neighbours)
@@ -187,6 +188,7 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   g.own = s.plane0[col];
   g.own_out = g.own;
   g.mir_lo = g.mir_hi = nullptr;
+  g.tstore = ctx->tune_tstore;
   g.oth = s.plane0[col ^ 1];
   g.ps = ctx->ps;
   g.pp = ctx->pp;
@@ -1593,6 +1595,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "fused_planes") ctx->tune_fused_xc = std::max(1, value);
   else if (n == "fused_debug") ctx->tune_fused_dbg = value;
   else if (n == "resident") ctx->tune_resident = value;
+  else if (n == "tma_store") ctx->tune_tstore = value;
   else if (n == "mirror_halo") ctx->tune_mirror = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;

@@ -1,0 +1,53 @@
+"""Interleaved A/B of a kgs_set_param knob on the fused colour passes
+(1 GPU, resident state): average live pass time per setting, and the fields
+must come out bitwise identical for every setting.
+
+    python tools/knob_ab.py KNOB V0,V1[,..] [--N 1024] [--steps 6] [--reps 4]
+"""
+import argparse
+import hashlib
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2502_09537_b200 as kgs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("knob")
+    ap.add_argument("values")
+    ap.add_argument("--N", type=int, default=1024)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--reps", type=int, default=4)
+    a = ap.parse_args()
+    vals = [int(v) for v in a.values.split(",")]
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(a.N)
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    times = {v: [] for v in vals}
+    digests = {}
+    for rep in range(a.reps):
+        for v in vals:
+            dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
+            dev.ctx.set_param(a.knob, v)
+            dev.ctx.pass_timing(True)
+            dev.ctx.step_dpavf2(args, a.steps, 0, a.steps)
+            n, ms, _ = dev.ctx.pass_stats()
+            times[v].append(ms / n)
+            if rep == 0:
+                h = hashlib.sha256()
+                st = dev.to_host()
+                for f in "PQUV":
+                    h.update(getattr(st, f).tobytes())
+                digests[v] = h.hexdigest()[:16]
+            dev.close()
+    out = {str(v): {"pass_ms": [round(t, 4) for t in times[v]],
+                    "mean": round(sum(times[v]) / len(times[v]), 4)} for v in vals}
+    out["bitwise_equal"] = len(set(digests.values())) == 1
+    print(json.dumps({"knob": a.knob, "N": a.N, **out}))
+
+
+if __name__ == "__main__":
+    main()
