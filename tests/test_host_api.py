@@ -102,6 +102,17 @@ def test_coefficients_errors_and_hand_inverse():
     assert (i00, i01, i10, i11) == pytest.approx((0.5, 0.5, -0.5, 0.5))
 
 
+def test_coefficients_inverse_identity_and_kappa1_zero():
+    """uv_inv inverts [[1, -tau/2], [c_uv, 1]]; kappa1 = 0 zeroes alpha, beta
+    (reference tests/test_integrator.py:34-44)."""
+    g = kgs.GridSpec(3, -1.0, 1.0, 6)
+    c = kgs.precompute_coefficients(kgs.PhysParams(0.3, 1.7, 0.9, 1.1), 0.05, g)
+    m = np.array([[1.0, -c.tau / 2], [c.c_uv, 1.0]])
+    assert np.allclose(np.array(c.uv_inv) @ m, np.eye(2), atol=1e-14)
+    c0 = kgs.precompute_coefficients(kgs.PhysParams(kappa1=0.0), 0.1, kgs.GridSpec(2, 0.0, 1.0, 8))
+    assert c0.alpha == 0.0 and c0.beta == 0.0
+
+
 def test_checkerboard_schedule_conventions():
     g = kgs.GridSpec(2, 0.0, 1.0, 4)
     with pytest.raises(ValueError, match="even N"):
