@@ -275,6 +275,9 @@ def run_ours(args):
         dev.download(host)
         dev.close()
         del dev
+        # untimed warm-up call (W steps): creates the cached context and its
+        # pipeline buffers, as the device timing's warm-up steps do
+        kgs.integrate(host, g, sc.params, sch, ex, TAU, W * TAU, record_stride=W)
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -285,7 +288,9 @@ def run_ours(args):
         e2e = {"value": updates / e2e_wall, "unit": UNIT,
                "h2d_bytes_per_step": state_bytes // K, "d2h_bytes_per_step": state_bytes // K,
                "wall_s": e2e_wall, "steps_per_call": K,
-               "note": "integrate(host pinned FieldState): upload + K steps + download per call"}
+               "note": "integrate(host pinned FieldState): upload + K steps + download in one "
+                       "call (pipelined: chunks stream in, passes follow as a wavefront, "
+                       "finished chunks stream out); one untimed warm-up call first"}
         kgs.clear_contexts()
     else:
         dev.close()

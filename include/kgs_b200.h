@@ -140,6 +140,24 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
                     int64_t step_offset, int64_t record_stride,
                     double* terms_out, int64_t* first_bad_step, int flags);
 
+/* A whole integrate() call on a HOST state (dpavf/integrator.py:147-182):
+ * upload P, Q, U, V, record the initial energy terms (terms0[8]), run
+ * `nsteps` DP-AVF2 steps recording every `record_stride` steps into
+ * terms_out[nrec][8] as kgs_step_dpavf2 does, and write the final state back
+ * into the same host arrays.  On one slab the upload, the colour passes and
+ * the download are overlapped as a pipeline (chunks of planes arrive around
+ * plane 0; every pass advances one plane behind its predecessor; finished
+ * chunks are copied back while later ones still compute -- page-locked host
+ * arrays give the overlap); otherwise, or without memory for the pipeline,
+ * the same result is produced by upload + kgs_step_dpavf2 + download.
+ * Fields are bitwise the same either way.  KGS_ENONFINITE: the host arrays
+ * hold the state after step *first_bad_step (replayed exactly), like the
+ * reference's integrate.  Knobs: "pipeline" (1/0), "pipeline_planes". */
+int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
+                       const kgs_coeffs* half, int64_t nsteps, int64_t step_offset,
+                       int64_t record_stride, double* terms0, double* terms_out,
+                       int64_t* first_bad_step, int flags);
+
 /* ---- diagnostics (dpavf/grid.py:152-187) ------------------------------- */
 
 /* Unscaled sums over this context's points, deterministic for a given

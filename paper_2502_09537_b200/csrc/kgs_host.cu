@@ -93,6 +93,14 @@ struct Slab {
   cudaEvent_t ev_xch = nullptr;     // last exchange into this slab's ghosts done
   bool xch_pending = false;
   cudaEvent_t ev_face[2] = {nullptr, nullptr};  // boundary planes of pass k written (k & 1)
+  // pipelined host integration (kgs_integrate_host)
+  cudaStream_t dstream = nullptr;   // downloads
+  double* pipe_up = nullptr;        // natural-layout staging, one chunk of 4 fields
+  double* pipe_dn = nullptr;
+  int64_t pipe_stage = 0;           // doubles per staging buffer
+  double* pipe_part = nullptr;      // per-record DIAG partials
+  int64_t pipe_part_cap = 0;
+  std::vector<cudaEvent_t> pipe_ev; // arrival / final events per chunk
 };
 
 }  // namespace
@@ -128,7 +136,9 @@ struct kgs_ctx {
   int tune_fused_xc = 128; // fused step: K4 planes per unit
   int tune_fused_dbg = 0;  // fused step timing experiments (results invalid)
   int tune_resident = 1;   // small grids: whole call in one launch (shared memory)
-  int tune_tstore = 2;     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
+  int tune_tstore = 2;
+  int tune_pipe = 1;         // kgs_integrate_host: overlap upload | passes | download
+  int tune_pipe_chunk = 32;  // planes per transfer chunk     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
   // fused halo exchange (single-process slabs): boundary launches
   // store their faces straight into the neighbours' ghost planes
   bool mirror = false;       // possible for this context (peer-accessible neighbours)
@@ -1199,6 +1209,12 @@ int kgs_destroy(kgs_ctx* ctx) {
     if (s.ev_xch) cudaEventDestroy(s.ev_xch);
     for (int i = 0; i < 2; ++i)
       if (s.ev_face[i]) cudaEventDestroy(s.ev_face[i]);
+    if (s.dstream) cudaStreamSynchronize(s.dstream);
+    for (auto e : s.pipe_ev) cudaEventDestroy(e);
+    if (s.dstream) cudaStreamDestroy(s.dstream);
+    if (s.pipe_up) cudaFree(s.pipe_up);
+    if (s.pipe_dn) cudaFree(s.pipe_dn);
+    if (s.pipe_part) cudaFree(s.pipe_part);
     if (s.cstream) cudaStreamDestroy(s.cstream);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
@@ -1252,6 +1268,256 @@ int transfer_planes(kgs_ctx* ctx, int fi, int64_t xg0, int64_t n, double* host, 
     CK(cudaStreamSynchronize(s.stream));
   }
   return KGS_OK;
+}
+
+// ---- pipelined host integration (kgs_integrate_host) ---------------------
+// Upload, the colour passes of a whole integrate() call and the download
+// overlap.  Chunks of C planes arrive in folded order (block 0, the last
+// block, block 1, the one before, ...), so the arrived region is a periodic
+// interval around plane 0 that grows on alternating sides.  Every pass reads
+// the other colour at x-1..x+1 and overwrites what its predecessor read, so
+// pass j may cover its predecessor's done region shrunk by one plane on each
+// side (RAW and WAR at once); the whole ring once the predecessor has it.
+// All passes therefore advance as a wavefront behind the upload, on the
+// compute stream in dependency order, and a C-plane block is downloaded
+// (merge kernel + D2H on a third stream) as soon as the last pass covered it:
+// H2D, compute and D2H proceed together (PCIe is full duplex).  The initial
+// state is also copied device-side (the second buffer set) so a non-finite
+// step can be replayed exactly.  Records get their own partial regions (the
+// DIAG passes of different steps are in flight together).
+int ensure_alt(kgs_ctx* ctx) {
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    const size_t colour_bytes = (size_t)(s.nx + 2) * ctx->ps * sizeof(double);
+    for (int c = 0; c < 2; ++c) {
+      if (s.alt[c]) continue;
+      if (cudaMalloc(&s.alt[c], colour_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        s.alt[c] = nullptr;
+        return KGS_ENOMEM;
+      }
+      s.alt0[c] = s.alt[c] + ctx->ps;
+    }
+  }
+  return KGS_OK;
+}
+
+struct PipePass {
+  int col, op1, op2;
+  bool diag, check;
+  int step_no;
+  int rec;      // record of its DIAG partials (-1: none)
+  int shrink;   // planes given up on each side relative to the predecessor
+};
+
+constexpr int kPipeFallback = 1;   // not eligible / no memory: use the plain path
+
+int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, int64_t nsteps,
+                        int64_t step_offset, int64_t record_stride, int64_t nrec,
+                        unsigned long long* bad_out) {
+  if (!ctx->tune_pipe || ctx->slabs.size() != 1 || ctx->dist || ctx->d != 3)
+    return kPipeFallback;
+  Slab& s = ctx->slabs[0];
+  const int64_t N = s.nx;
+  const int64_t C = std::max<int64_t>(1, ctx->tune_pipe_chunk);
+  const int64_t nb = (N + C - 1) / C;
+  if (nb < 4) return kPipeFallback;
+  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
+  CK(cudaSetDevice(s.dev));
+  if (ensure_alt(ctx)) return kPipeFallback;
+  const int64_t stage = 4 * C * nat_plane;
+  if (s.pipe_stage < stage) {
+    if (s.pipe_up) CK(cudaFree(s.pipe_up));
+    if (s.pipe_dn) CK(cudaFree(s.pipe_dn));
+    s.pipe_up = s.pipe_dn = nullptr;
+    s.pipe_stage = 0;
+    if (cudaMalloc(&s.pipe_up, stage * 8) != cudaSuccess ||
+        cudaMalloc(&s.pipe_dn, stage * 8) != cudaSuccess) {
+      cudaGetLastError();
+      if (s.pipe_up) cudaFree(s.pipe_up);
+      s.pipe_up = nullptr;
+      return kPipeFallback;
+    }
+    s.pipe_stage = stage;
+  }
+  const int64_t maxl = nb + 4;                                 // launches per pass
+  const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
+  const int64_t need = (nrec + 1) * 2 * region;
+  if (s.pipe_part_cap < need) {
+    if (need > (int64_t)1 << 27) return kPipeFallback;         // > 1 GiB of partials
+    if (s.pipe_part) CK(cudaFree(s.pipe_part));
+    s.pipe_part = nullptr;
+    s.pipe_part_cap = 0;
+    if (cudaMalloc(&s.pipe_part, need * 8) != cudaSuccess) {
+      cudaGetLastError();
+      return kPipeFallback;
+    }
+    s.pipe_part_cap = need;
+  }
+  if (!s.dstream) CK(cudaStreamCreateWithFlags(&s.dstream, cudaStreamNonBlocking));
+  while ((int64_t)s.pipe_ev.size() < 2 * nb) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s.pipe_ev.push_back(e);
+  }
+  int r = ensure_records(ctx, nrec + 1);
+  if (!r) r = reset_bad(ctx);
+  if (r) return r;
+  ctx->pending = false;   // the whole state is replaced
+
+  // the passes of the call: initial energy (black self, red edges + self),
+  // head, then K3(n), K4(n) per step (K4 of the last step = the tail)
+  std::vector<PipePass> passes;
+  passes.push_back({0, OP_NONE, OP_NONE, true, false, 0, 0, 0});
+  passes.push_back({1, OP_NONE, OP_NONE, true, false, 0, 0, 1});
+  passes.push_back({1, OP_BASE, OP_NONE, false, false, 0, -1, 0});
+  int64_t slot = 0;
+  for (int64_t i = 1; i <= nsteps; ++i) {
+    const int64_t n = step_offset + i;
+    const bool rec = record_stride > 0 && n % record_stride == 0;
+    const int rid = rec ? (int)(1 + slot++) : -1;
+    passes.push_back({0, OP_BASE, OP_ADJ, rec, true, (int)n, rid, 1});
+    passes.push_back({1, OP_ADJ, i < nsteps ? OP_BASE : OP_NONE, rec, true, (int)n, rid, 1});
+  }
+  const int J = (int)passes.size();
+  std::vector<int64_t> lo(J, 0), hi(J, 0);   // done regions, unwrapped: lo <= 0 <= hi
+  std::vector<char> full(J, 0);
+  std::vector<int64_t> roff((size_t)(nrec + 1) * 2, 0);
+
+  auto launch_range = [&](const PipePass& P, int64_t xa, int64_t xb) -> int {
+    if (xb <= xa) return KGS_OK;
+    double* save = s.partials[P.col];
+    const int64_t ri = P.diag ? (int64_t)P.rec * 2 + P.col : 0;
+    if (P.diag) {
+      s.partials[P.col] = s.pipe_part + ri * region;
+      s.npart[P.col] = (int)roff[ri];
+    }
+    int rr = launch_pass(ctx, s, P.col, P.op1, P.op2, P.diag, P.check, c, P.step_no, (int)xa,
+                         (int)xb);
+    if (P.diag) {
+      roff[ri] = s.npart[P.col];
+      s.partials[P.col] = save;
+    }
+    return rr;
+  };
+  auto launch_u = [&](const PipePass& P, int64_t u0, int64_t u1) -> int {  // unwrapped range
+    if (u1 <= u0) return KGS_OK;
+    if (u1 <= 0) return launch_range(P, N + u0, N + u1);
+    if (u0 >= 0) return launch_range(P, u0, u1);
+    int rr = launch_range(P, N + u0, N);
+    return rr ? rr : launch_range(P, 0, u1);
+  };
+
+  CK(cudaEventRecord(s.ev_t0, s.cstream));
+  // uploads (folded block order) on the comm stream: H2D, split, backup copy
+  std::vector<int64_t> order(nb);
+  for (int64_t m = 0; m < nb; ++m) order[m] = (m % 2 == 0) ? m / 2 : nb - 1 - m / 2;
+  for (int64_t m = 0; m < nb; ++m) {
+    const int64_t x0 = order[m] * C, x1 = std::min(N, x0 + C), nxc = x1 - x0;
+    for (int f = 0; f < 4; ++f)
+      CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + x0 * nat_plane,
+                         (size_t)nxc * nat_plane * 8, cudaMemcpyHostToDevice, s.cstream));
+    const int64_t cnt = nxc * ctx->ny * ctx->nk;
+    const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
+    for (int f = 0; f < 4; ++f) {
+      PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
+      g.own += f * ctx->pp;
+      g.oth += f * ctx->pp;
+      split_field<<<blocks, 256, 0, s.cstream>>>(s.pipe_up + f * C * nat_plane, g, (int)nxc,
+                                                  (int)x0);
+      ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    for (int cc = 0; cc < 2; ++cc)
+      CK(cudaMemcpyAsync(s.alt0[cc] + x0 * ctx->ps, s.plane0[cc] + x0 * ctx->ps,
+                         (size_t)nxc * ctx->ps * 8, cudaMemcpyDeviceToDevice, s.cstream));
+    CK(cudaEventRecord(s.pipe_ev[m], s.cstream));
+  }
+
+  // the wavefront on the compute stream; downloads behind it
+  std::vector<char> dl(nb, 0);
+  int64_t alo = 0, ahi = 0;
+  for (int64_t m = 0; m < nb && !r; ++m) {
+    CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[m], 0));
+    const int64_t x0 = order[m] * C, x1 = std::min(N, x0 + C);
+    if (m % 2 == 0) ahi = x1; else alo = x0 - N;
+    const bool afull = m == nb - 1;
+    int64_t plo = alo, phi = ahi;
+    bool pfull = afull;
+    for (int j = 0; j < J && !r; ++j) {
+      const PipePass& P = passes[j];
+      if (!full[j]) {
+        if (pfull) {
+          if (lo[j] == hi[j]) r = launch_range(P, 0, N);
+          else r = launch_range(P, hi[j], N + lo[j]);
+          full[j] = 1;
+        } else {
+          const int64_t nlo = plo + P.shrink, nhi = phi - P.shrink;
+          if (nhi > nlo) {
+            if (lo[j] == hi[j]) r = launch_u(P, nlo, nhi);
+            else {
+              r = launch_u(P, nlo, lo[j]);
+              if (!r) r = launch_u(P, hi[j], nhi);
+            }
+            lo[j] = nlo;
+            hi[j] = nhi;
+          }
+        }
+      }
+      pfull = full[j];
+      plo = lo[j];
+      phi = hi[j];
+    }
+    // download the blocks the last pass has finished
+    for (int64_t k = 0; k < nb && !r; ++k) {
+      if (dl[k]) continue;
+      const int64_t b0 = k * C, b1 = std::min(N, b0 + C);
+      // the whole block inside the last pass's done region [lo, hi) (unwrapped;
+      // it need not contain plane 0 yet)
+      const int64_t L = lo[J - 1], H = hi[J - 1];
+      const bool fin = full[J - 1] ||
+                       (L < H && ((b0 >= L && b1 <= H) || (b0 - N >= L && b1 - N <= H)));
+      if (!fin) continue;
+      dl[k] = 1;
+      cudaEvent_t ev = s.pipe_ev[nb + k];
+      CK(cudaEventRecord(ev, s.stream));
+      CK(cudaStreamWaitEvent(s.dstream, ev, 0));
+      const int64_t nxc = b1 - b0;
+      const int64_t cnt = nxc * ctx->ny * ctx->nk;
+      const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
+      for (int f = 0; f < 4; ++f) {
+        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
+        g.own += f * ctx->pp;
+        g.oth += f * ctx->pp;
+        merge_field<<<blocks, 256, 0, s.dstream>>>(s.pipe_dn + f * C * nat_plane, g, (int)nxc,
+                                                    (int)b0);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(host[f] + b0 * nat_plane, s.pipe_dn + f * C * nat_plane,
+                           (size_t)nxc * nat_plane * 8, cudaMemcpyDeviceToHost, s.dstream));
+      }
+      CK(cudaGetLastError());
+    }
+  }
+  if (r) return r;
+  for (int64_t k = 0; k < nb; ++k)
+    if (!dl[k]) return fail(ctx, KGS_ECUDA, "pipeline left block %lld undownloaded", (long long)k);
+  for (int64_t q = 0; q <= nrec; ++q) {
+    finalize_terms<<<1, kThreads, 0, s.stream>>>(
+        s.pipe_part + (q * 2 + 1) * region, (int)roff[q * 2 + 1], s.pipe_part + (q * 2) * region,
+        (int)roff[q * 2], s.records + q * NTERMS);
+    ctx->launches++;
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s.ev_done, s.dstream));
+  CK(cudaStreamWaitEvent(s.stream, s.ev_done, 0));
+  CK(cudaEventRecord(s.ev_t1, s.stream));
+  r = sync_all(ctx);
+  if (!r) CK(cudaStreamSynchronize(s.dstream));
+  if (r) return r;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, s.ev_t0, s.ev_t1));
+  ctx->last_ms = ms;
+  return read_bad(ctx, bad_out);
 }
 
 int check_range(kgs_ctx* ctx, int field, int64_t xg0, int64_t n, const void* p) {
@@ -1460,6 +1726,73 @@ int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
   return KGS_OK;
 }
 
+int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
+                       const kgs_coeffs* half, int64_t nsteps, int64_t step_offset,
+                       int64_t record_stride, double* terms0, double* terms_out,
+                       int64_t* first_bad_step, int flags) {
+  (void)flags;
+  if (!ctx || !P || !Q || !U || !V || !half || !terms0)
+    return fail(ctx, KGS_EINVAL, "NULL argument");
+  if (nsteps < 0 || record_stride < 0 || step_offset < 0)
+    return fail(ctx, KGS_EINVAL, "negative nsteps/step_offset/record_stride");
+  if (nsteps + step_offset > INT_MAX) return fail(ctx, KGS_EINVAL, "step numbers too large");
+  if (first_bad_step) *first_bad_step = 0;
+  const int64_t nrec = record_stride > 0
+      ? (step_offset + nsteps) / record_stride - step_offset / record_stride : 0;
+  if (nrec > 0 && !terms_out) return fail(ctx, KGS_EINVAL, "terms_out is NULL");
+  double* host[4] = {P, Q, U, V};
+  const Coeffs c = to_coeffs(half);
+  unsigned long long bad = ULLONG_MAX;
+  int r = nsteps > 0 ? integrate_pipelined(ctx, host, c, nsteps, step_offset, record_stride,
+                                          nrec, &bad)
+                     : kPipeFallback;
+  if (r == kPipeFallback) {
+    // plain path: upload, initial energy, steps, download
+    r = kgs_upload(ctx, P, Q, U, V);
+    if (!r) r = kgs_energy_terms(ctx, terms0);
+    if (r) return r;
+    int64_t fb = 0;
+    r = kgs_step_dpavf2(ctx, half, nsteps, step_offset, record_stride, terms_out, &fb, 0);
+    if (r && r != KGS_ENONFINITE) return r;
+    if (r == KGS_ENONFINITE) {   // replay from the (untouched) host state to the bad step
+      int r2 = kgs_upload(ctx, P, Q, U, V);
+      int64_t fb2 = 0;
+      if (!r2 && fb > step_offset)
+        r2 = kgs_step_dpavf2(ctx, half, fb - step_offset, step_offset, 0, nullptr, &fb2, 0);
+      if (r2 && r2 != KGS_ENONFINITE) return r2;
+      if (first_bad_step) *first_bad_step = fb;
+      int r3 = kgs_download(ctx, P, Q, U, V);
+      if (r3) return r3;
+      return fail(ctx, KGS_ENONFINITE, "non-finite field values detected after step %lld",
+                  (long long)fb);
+    }
+    return kgs_download(ctx, P, Q, U, V);
+  }
+  if (r) return r;
+  Slab& s = ctx->slabs[0];
+  std::vector<double> rec((size_t)(nrec + 1) * NTERMS);
+  CK(cudaMemcpy(rec.data(), s.records, rec.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  std::copy(rec.begin(), rec.begin() + NTERMS, terms0);
+  if (nrec > 0) std::copy(rec.begin() + NTERMS, rec.end(), terms_out);
+  if (bad != ULLONG_MAX) {
+    // restore the initial state (device copy) and replay exactly to the bad step
+    for (int cc = 0; cc < 2; ++cc)
+      CK(cudaMemcpy(s.buf[cc], s.alt[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
+                    cudaMemcpyDeviceToDevice));
+    int64_t fb2 = 0;
+    r = KGS_OK;
+    if ((int64_t)bad > step_offset)
+      r = kgs_step_dpavf2(ctx, half, (int64_t)bad - step_offset, step_offset, 0, nullptr, &fb2,
+                          0);
+    if (r && r != KGS_ENONFINITE) return r;
+    r = kgs_download(ctx, P, Q, U, V);
+    if (r) return r;
+    if (first_bad_step) *first_bad_step = (int64_t)bad;
+    return fail(ctx, KGS_ENONFINITE, "non-finite field values detected after step %llu", bad);
+  }
+  return KGS_OK;
+}
+
 int kgs_energy_mass(kgs_ctx* ctx, double kappa1, double kappa2, double mu,
                     double gamma, double* E, double* mass) {
   double t[NTERMS];
@@ -1596,6 +1929,8 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "fused_debug") ctx->tune_fused_dbg = value;
   else if (n == "resident") ctx->tune_resident = value;
   else if (n == "tma_store") ctx->tune_tstore = value;
+  else if (n == "pipeline") ctx->tune_pipe = value;
+  else if (n == "pipeline_planes") ctx->tune_pipe_chunk = std::max(1, value);
   else if (n == "mirror_halo") ctx->tune_mirror = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;

@@ -173,6 +173,26 @@ class DeviceContext:
         c = _lib.coeffs_struct(kernel_args)
         self.check(_lib.load().kgs_sweep(self.ptr, colour, kind, ctypes.byref(c)))
 
+    def integrate_host(self, state, kernel_args, nsteps: int, record_stride: int = 0):
+        """One call for a whole host-state integration (kgs_integrate_host):
+        upload, nsteps DP-AVF2 steps and download overlapped in a pipeline;
+        the host arrays are updated in place.  Returns (terms0, terms[nrec, 8],
+        bad_step); on a non-finite step the state is the one after `bad_step`."""
+        if self.dist:
+            raise ValueError("integrate_host is for single-process contexts")
+        lib = _lib.load()
+        c = _lib.coeffs_struct(kernel_args)
+        nrec = nsteps // record_stride if record_stride > 0 else 0
+        terms0 = np.zeros(_lib.NTERMS)
+        terms = np.zeros((max(nrec, 1), _lib.NTERMS))
+        bad = ctypes.c_int64(0)
+        rc = lib.kgs_integrate_host(self.ptr, *(_lib.dptr(getattr(state, f)) for f in "PQUV"),
+                                    ctypes.byref(c), nsteps, 0, record_stride,
+                                    _lib.dptr(terms0), _lib.dptr(terms), ctypes.byref(bad), 0)
+        if rc not in (_lib.KGS_OK, _lib.KGS_ENONFINITE):
+            self.check(rc)
+        return terms0, terms[:nrec], (bad.value if rc == _lib.KGS_ENONFINITE else 0)
+
     def step_dpavf2(self, kernel_args, nsteps: int, step_offset: int = 0,
                     record_stride: int = 0, defer_tail: bool = False):
         """Run nsteps fused DP-AVF2 steps; returns (terms[nrec, 8], bad_step).

@@ -22,7 +22,9 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
-from .device import DeviceFieldState, as_device_state
+import numpy as np
+
+from .device import DeviceFieldState, as_device_state, get_context
 from .grid import FieldState, GridSpec, PhysParams, energy_from_terms
 from .ordering import BLACK, RED, UpdateSchedule, require_checkerboard
 
@@ -136,6 +138,29 @@ class EnergyTrace:
         return max(self.rel_error)
 
 
+def _pipeline_ok(host) -> bool:
+    return all(getattr(host, f).dtype == np.float64 and getattr(host, f).flags["C_CONTIGUOUS"]
+               for f in "PQUV")
+
+
+def _append_records(trace, terms, k0, k1, record_stride, t, e0, absolute, params, grid,
+                    advance_t) -> float:
+    """Append the records of steps k0..k1 (every record_stride-th) from the
+    device term sums; returns t after step k1."""
+    rec = iter(terms)
+    for k in range(k0, k1 + 1):
+        t = advance_t(t, 1)
+        if k % record_stride == 0:
+            e, m = energy_from_terms(next(rec), params, grid)
+            re = abs(e - e0) if absolute else abs(e - e0) / abs(e0)
+            trace.steps.append(k)
+            trace.times.append(t)
+            trace.energy.append(e)
+            trace.rel_error.append(re)
+            trace.mass.append(m)
+    return t
+
+
 def integrate(state, grid: GridSpec, params: PhysParams,
               schedule, executor, tau: float, T: float,
               record_stride: int = 1, snapshot_stride: int = 0,
@@ -160,11 +185,7 @@ def integrate(state, grid: GridSpec, params: PhysParams,
     args = coeffs_half.kernel_args()
 
     host = None if isinstance(state, DeviceFieldState) else state
-    dev, _ = as_device_state(state, grid, executor)
-
-    e0, m0 = energy_from_terms(dev.energy_terms(), params, grid)
-    absolute = abs(e0) < 1e-300
-    trace = EnergyTrace([0], [state.t], [e0], [0.0], [m0], re_is_absolute=absolute)
+    snap = snapshot_stride if (snapshot_stride and snapshot_writer) else 0
 
     def advance_t(t: float, k: int) -> float:
         for _ in range(k):       # t += tau/2 twice per step, like the reference
@@ -172,8 +193,30 @@ def integrate(state, grid: GridSpec, params: PhysParams,
             t += coeffs_half.tau
         return t
 
+    if host is not None and not snap and n_steps > 0 and _pipeline_ok(host):
+        ctx = get_context(grid, executor)
+        if not ctx.dist:
+            # one call: upload | steps | download overlapped (kgs_integrate_host)
+            t_start = state.t
+            terms0, terms, bad = ctx.integrate_host(host, args, n_steps, record_stride)
+            e0, m0 = energy_from_terms(terms0, params, grid)
+            absolute = abs(e0) < 1e-300
+            trace = EnergyTrace([0], [t_start], [e0], [0.0], [m0], re_is_absolute=absolute)
+            if bad:
+                state.t = advance_t(t_start, bad)
+                raise FloatingPointError(
+                    f"non-finite field values detected after step {bad} (t={state.t})")
+            state.t = _append_records(trace, terms, 1, n_steps, record_stride, t_start, e0,
+                                      absolute, params, grid, advance_t)
+            return trace
+
+    dev, _ = as_device_state(state, grid, executor)
+
+    e0, m0 = energy_from_terms(dev.energy_terms(), params, grid)
+    absolute = abs(e0) < 1e-300
+    trace = EnergyTrace([0], [state.t], [e0], [0.0], [m0], re_is_absolute=absolute)
+
     # chunk boundaries: snapshot steps (the host state is synced there)
-    snap = snapshot_stride if (snapshot_stride and snapshot_writer) else 0
     n = 0
     while n < n_steps:
         n1 = n_steps if not snap else min(n_steps, (n // snap + 1) * snap)
@@ -188,19 +231,8 @@ def integrate(state, grid: GridSpec, params: PhysParams,
             state.t = advance_t(t_start, bad - n)
             raise FloatingPointError(
                 f"non-finite field values detected after step {bad} (t={state.t})")
-        t = t_start
-        rec = iter(terms)
-        for k in range(n + 1, n1 + 1):
-            t = advance_t(t, 1)
-            if k % record_stride == 0:
-                e, m = energy_from_terms(next(rec), params, grid)
-                re = abs(e - e0) if absolute else abs(e - e0) / abs(e0)
-                trace.steps.append(k)
-                trace.times.append(t)
-                trace.energy.append(e)
-                trace.rel_error.append(re)
-                trace.mass.append(m)
-        state.t = t
+        state.t = _append_records(trace, terms, n + 1, n1, record_stride, t_start, e0,
+                                  absolute, params, grid, advance_t)
         n = n1
         if snap and n % snap == 0:
             if host is not None:

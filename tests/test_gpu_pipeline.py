@@ -1,0 +1,89 @@
+"""kgs_integrate_host: upload | colour passes | download as one pipeline
+(chunks of planes arrive around plane 0, every pass advances one plane
+behind its predecessor, finished chunks go back while later ones compute).
+Bitwise the plain upload + steps + download path, for any chunk size."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2502_09537_b200 as kgs
+from conftest import assert_bitwise
+from paper_2502_09537_b200.device import get_context
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(g, sc, s0, tau, T, stride, pipeline, planes=32):
+    ctx = get_context(g, None)
+    ctx.set_param("pipeline", pipeline)
+    ctx.set_param("pipeline_planes", planes)
+    s = s0.copy()
+    tr = kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, tau, T,
+                       record_stride=stride)
+    ctx.set_param("pipeline", 1)
+    ctx.set_param("pipeline_planes", 32)
+    return s, tr
+
+
+@pytest.mark.parametrize("N,steps,stride,planes", [
+    (128, 5, 1, 32), (128, 7, 3, 8), (128, 4, 4, 5), (192, 3, 2, 16), (256, 6, 6, 32),
+    (128, 1, 1, 32), (64, 9, 2, 4), (128, 1, 1, 3), (128, 2, 1, 6), (128, 3, 3, 7)])
+def test_pipeline_bitwise_vs_plain_and_oracle(N, steps, stride, planes):
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(N)
+    s0 = sc.state(g)
+    tau = 0.01
+    a, ta = _run(g, sc, s0, tau, steps * tau, stride, 1, planes)
+    b, tb = _run(g, sc, s0, tau, steps * tau, stride, 0, planes)
+    assert_bitwise(a, b)
+    assert a.t == b.t and ta.steps == tb.steps and ta.times == tb.times
+    np.testing.assert_allclose(ta.energy, tb.energy, rtol=1e-13, atol=0)
+    np.testing.assert_allclose(ta.mass, tb.mass, rtol=1e-13, atol=0)
+    assert ta.max_rel_error() < 1e-12
+    if N <= 128:
+        ref = s0.copy()
+        oracle.CheckerboardOracle(3, N).step_dpavf2(
+            ref, oracle.kernel_args(sc.params, tau / 2, g), steps,
+            workers=oracle.CheckerboardOracle.max_threads())
+        assert_bitwise(a, ref)
+
+
+@pytest.mark.parametrize("bad_plane", [0, 63, 127])
+def test_pipeline_nonfinite_replays_to_the_bad_step(bad_plane):
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    i = bad_plane * 128 * 128 + 77
+    s0.U[i] = np.inf
+    outs = []
+    for pipeline in (1, 0):
+        s = s0.copy()
+        ctx = get_context(g, None)
+        ctx.set_param("pipeline", pipeline)
+        with pytest.raises(FloatingPointError, match="after step 1"):
+            kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, 0.01, 0.05)
+        outs.append(s)
+    get_context(g, None).set_param("pipeline", 1)
+    assert outs[0].t == outs[1].t
+    for f in "PQUV":
+        np.testing.assert_array_equal(getattr(outs[0], f), getattr(outs[1], f))
+
+
+def test_pipeline_device_state_after_call_is_the_result():
+    """The context keeps the final state resident: a following resident step
+    continues from it exactly."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    s = s0.copy()
+    kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, 0.01, 0.04)
+    ref = s0.copy()
+    oracle.CheckerboardOracle(3, 128).step_dpavf2(
+        ref, oracle.kernel_args(sc.params, 0.005, g), 4,
+        workers=oracle.CheckerboardOracle.max_threads())
+    assert_bitwise(s, ref)
+    z = kgs.FieldState.zeros(g)
+    get_context(g, None).download(z)
+    assert_bitwise(z, ref)
