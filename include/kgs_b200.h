@@ -158,6 +158,15 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
                        int64_t record_stride, double* terms0, double* terms_out,
                        int64_t* first_bad_step, int flags);
 
+/* The schedule kgs_integrate_host executes for N planes, chunks of C planes
+ * and nsteps steps, as events (kind, index, a, b) written to out[4 * i ..]
+ * (at most `cap` events): kind 0 = chunk `index` (planes [a, b)) arrived,
+ * 1 = pass `index` over planes [a, b) (passes: 0 black energy terms, 1 red
+ * energy terms, 2 head, then K3/K4 per step), 2 = block `index` (planes
+ * [a, b)) final and copied back.  Pure host logic (no device); returns the
+ * number of events, -1 on bad arguments. */
+int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap);
+
 /* ---- diagnostics (dpavf/grid.py:152-187) ------------------------------- */
 
 /* Unscaled sums over this context's points, deterministic for a given

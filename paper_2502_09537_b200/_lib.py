@@ -28,7 +28,8 @@ KGS_STEP_DEFER_TAIL = 1
 EXPORTED = (
     "kgs_create", "kgs_create_dist", "kgs_nccl_unique_id", "kgs_destroy",
     "kgs_local_range", "kgs_upload", "kgs_download", "kgs_sweep",
-    "kgs_step_dpavf2", "kgs_integrate_host", "kgs_energy_terms", "kgs_energy_mass",
+    "kgs_step_dpavf2", "kgs_integrate_host", "kgs_pipeline_plan", "kgs_energy_terms",
+    "kgs_energy_mass",
     "kgs_all_finite", "kgs_last_error", "kgs_launch_count",
     "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version",
     "kgs_pass_timing", "kgs_pass_stats", "kgs_host_alloc", "kgs_host_free",
@@ -90,6 +91,7 @@ def load() -> ctypes.CDLL:
         "kgs_integrate_host": (ctypes.c_int, [_P, _DP, _DP, _DP, _DP, ctypes.POINTER(KgsCoeffs),
                                               _I64, _I64, _I64, _DP, _DP,
                                               ctypes.POINTER(_I64), ctypes.c_int]),
+        "kgs_pipeline_plan": (_I64, [_I64, _I64, _I64, ctypes.POINTER(_I64), _I64]),
         "kgs_energy_terms": (ctypes.c_int, [_P, _DP]),
         "kgs_energy_mass": (ctypes.c_int, [_P, _D, _D, _D, _D, _DP, _DP]),
         "kgs_all_finite": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),

@@ -1312,6 +1312,82 @@ struct PipePass {
 
 constexpr int kPipeFallback = 1;   // not eligible / no memory: use the plain path
 
+// The pipeline as a list of events, in the order they are issued on the
+// compute stream: ARRIVE (wait for chunk m = planes [a, b)), PASS (pass j
+// over planes [a, b)), FINAL (planes [a, b) are final: copy them back).
+// Pure host logic (kgs_pipeline_plan exports it for the CPU tests).
+enum PipeKind : int { PIPE_ARRIVE = 0, PIPE_PASS = 1, PIPE_FINAL = 2 };
+struct PipeEvent {
+  int kind, pass;
+  int64_t a, b;
+};
+
+std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int>& shrink) {
+  std::vector<PipeEvent> ev;
+  const int64_t nb = (N + C - 1) / C;
+  const int J = (int)shrink.size();
+  std::vector<int64_t> lo(J, 0), hi(J, 0);   // done regions, unwrapped: empty or lo < hi
+  std::vector<char> full(J, 0), dl(nb, 0);
+  auto pass = [&](int j, int64_t a, int64_t b) {
+    if (b > a) ev.push_back({PIPE_PASS, j, a, b});
+  };
+  auto pass_u = [&](int j, int64_t u0, int64_t u1) {   // unwrapped range, u1 - u0 <= N
+    if (u1 <= u0) return;
+    while (u0 < 0) { u0 += N; u1 += N; }
+    while (u0 >= N) { u0 -= N; u1 -= N; }
+    if (u1 <= N) pass(j, u0, u1);
+    else { pass(j, u0, N); pass(j, 0, u1 - N); }
+  };
+  int64_t alo = 0, ahi = 0;
+  for (int64_t m = 0; m < nb; ++m) {
+    const int64_t blk = (m % 2 == 0) ? m / 2 : nb - 1 - m / 2;   // folded order
+    const int64_t x0 = blk * C, x1 = std::min(N, x0 + C);
+    ev.push_back({PIPE_ARRIVE, (int)m, x0, x1});
+    if (m % 2 == 0) ahi = x1; else alo = x0 - N;
+    int64_t plo = alo, phi = ahi;
+    bool pfull = m == nb - 1;
+    for (int j = 0; j < J; ++j) {
+      if (!full[j]) {
+        if (pfull) {   // the rest of the ring; the region need not contain plane 0
+          if (lo[j] == hi[j]) pass(j, 0, N);
+          else pass_u(j, hi[j], lo[j] + N);
+          full[j] = 1;
+        } else {
+          const int64_t nlo = plo + shrink[j], nhi = phi - shrink[j];
+          if (nhi > nlo) {
+            if (lo[j] == hi[j]) pass_u(j, nlo, nhi);
+            else { pass_u(j, nlo, lo[j]); pass_u(j, hi[j], nhi); }
+            lo[j] = nlo;
+            hi[j] = nhi;
+          }
+        }
+      }
+      pfull = full[j];
+      plo = lo[j];
+      phi = hi[j];
+    }
+    // blocks wholly inside the last pass's done region (which need not
+    // contain plane 0 yet) are final
+    const int64_t L = lo[J - 1], H = hi[J - 1];
+    for (int64_t k = 0; k < nb; ++k) {
+      if (dl[k]) continue;
+      const int64_t b0 = k * C, b1 = std::min(N, b0 + C);
+      if (full[J - 1] || (L < H && ((b0 >= L && b1 <= H) || (b0 - N >= L && b1 - N <= H)))) {
+        dl[k] = 1;
+        ev.push_back({PIPE_FINAL, (int)k, b0, b1});
+      }
+    }
+  }
+  return ev;
+}
+
+std::vector<int> pipeline_shrinks(int64_t nsteps) {
+  // initial energy (black self, red edges + self), head, then K3/K4 per step
+  std::vector<int> sh = {0, 1, 0};
+  for (int64_t i = 0; i < 2 * nsteps; ++i) sh.push_back(1);
+  return sh;
+}
+
 int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, int64_t nsteps,
                         int64_t step_offset, int64_t record_stride, int64_t nrec,
                         unsigned long long* bad_out) {
@@ -1380,9 +1456,10 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     passes.push_back({1, OP_ADJ, i < nsteps ? OP_BASE : OP_NONE, rec, true, (int)n, rid, 1});
   }
   const int J = (int)passes.size();
-  std::vector<int64_t> lo(J, 0), hi(J, 0);   // done regions, unwrapped: lo <= 0 <= hi
-  std::vector<char> full(J, 0);
   std::vector<int64_t> roff((size_t)(nrec + 1) * 2, 0);
+  std::vector<int> shrink(J);
+  for (int j = 0; j < J; ++j) shrink[j] = passes[j].shrink;
+  const std::vector<PipeEvent> plan = pipeline_plan(N, C, shrink);
 
   auto launch_range = [&](const PipePass& P, int64_t xa, int64_t xb) -> int {
     if (xb <= xa) return KGS_OK;
@@ -1400,20 +1477,12 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     }
     return rr;
   };
-  auto launch_u = [&](const PipePass& P, int64_t u0, int64_t u1) -> int {  // unwrapped range
-    if (u1 <= u0) return KGS_OK;
-    if (u1 <= 0) return launch_range(P, N + u0, N + u1);
-    if (u0 >= 0) return launch_range(P, u0, u1);
-    int rr = launch_range(P, N + u0, N);
-    return rr ? rr : launch_range(P, 0, u1);
-  };
 
   CK(cudaEventRecord(s.ev_t0, s.cstream));
   // uploads (folded block order) on the comm stream: H2D, split, backup copy
-  std::vector<int64_t> order(nb);
-  for (int64_t m = 0; m < nb; ++m) order[m] = (m % 2 == 0) ? m / 2 : nb - 1 - m / 2;
-  for (int64_t m = 0; m < nb; ++m) {
-    const int64_t x0 = order[m] * C, x1 = std::min(N, x0 + C), nxc = x1 - x0;
+  for (const PipeEvent& e : plan) {
+    if (e.kind != PIPE_ARRIVE) continue;
+    const int64_t m = e.pass, x0 = e.a, x1 = e.b, nxc = x1 - x0;
     for (int f = 0; f < 4; ++f)
       CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + x0 * nat_plane,
                          (size_t)nxc * nat_plane * 8, cudaMemcpyHostToDevice, s.cstream));
@@ -1435,54 +1504,19 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   }
 
   // the wavefront on the compute stream; downloads behind it
-  std::vector<char> dl(nb, 0);
-  int64_t alo = 0, ahi = 0;
-  for (int64_t m = 0; m < nb && !r; ++m) {
-    CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[m], 0));
-    const int64_t x0 = order[m] * C, x1 = std::min(N, x0 + C);
-    if (m % 2 == 0) ahi = x1; else alo = x0 - N;
-    const bool afull = m == nb - 1;
-    int64_t plo = alo, phi = ahi;
-    bool pfull = afull;
-    for (int j = 0; j < J && !r; ++j) {
-      const PipePass& P = passes[j];
-      if (!full[j]) {
-        if (pfull) {
-          if (lo[j] == hi[j]) r = launch_range(P, 0, N);
-          else r = launch_range(P, hi[j], N + lo[j]);
-          full[j] = 1;
-        } else {
-          const int64_t nlo = plo + P.shrink, nhi = phi - P.shrink;
-          if (nhi > nlo) {
-            if (lo[j] == hi[j]) r = launch_u(P, nlo, nhi);
-            else {
-              r = launch_u(P, nlo, lo[j]);
-              if (!r) r = launch_u(P, hi[j], nhi);
-            }
-            lo[j] = nlo;
-            hi[j] = nhi;
-          }
-        }
-      }
-      pfull = full[j];
-      plo = lo[j];
-      phi = hi[j];
-    }
-    // download the blocks the last pass has finished
-    for (int64_t k = 0; k < nb && !r; ++k) {
-      if (dl[k]) continue;
-      const int64_t b0 = k * C, b1 = std::min(N, b0 + C);
-      // the whole block inside the last pass's done region [lo, hi) (unwrapped;
-      // it need not contain plane 0 yet)
-      const int64_t L = lo[J - 1], H = hi[J - 1];
-      const bool fin = full[J - 1] ||
-                       (L < H && ((b0 >= L && b1 <= H) || (b0 - N >= L && b1 - N <= H)));
-      if (!fin) continue;
-      dl[k] = 1;
+  int64_t ndl = 0;
+  for (const PipeEvent& e : plan) {
+    if (r) break;
+    if (e.kind == PIPE_ARRIVE) {
+      CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[e.pass], 0));
+    } else if (e.kind == PIPE_PASS) {
+      r = launch_range(passes[e.pass], e.a, e.b);
+    } else {
+      const int64_t k = e.pass, b0 = e.a, nxc = e.b - e.a;
+      ++ndl;
       cudaEvent_t ev = s.pipe_ev[nb + k];
       CK(cudaEventRecord(ev, s.stream));
       CK(cudaStreamWaitEvent(s.dstream, ev, 0));
-      const int64_t nxc = b1 - b0;
       const int64_t cnt = nxc * ctx->ny * ctx->nk;
       const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
       for (int f = 0; f < 4; ++f) {
@@ -1499,8 +1533,8 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     }
   }
   if (r) return r;
-  for (int64_t k = 0; k < nb; ++k)
-    if (!dl[k]) return fail(ctx, KGS_ECUDA, "pipeline left block %lld undownloaded", (long long)k);
+  if (ndl != nb) return fail(ctx, KGS_ECUDA, "pipeline copied back %lld of %lld blocks",
+                             (long long)ndl, (long long)nb);
   for (int64_t q = 0; q <= nrec; ++q) {
     finalize_terms<<<1, kThreads, 0, s.stream>>>(
         s.pipe_part + (q * 2 + 1) * region, (int)roff[q * 2 + 1], s.pipe_part + (q * 2) * region,
@@ -1724,6 +1758,19 @@ int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
     for (int q = 0; q < NTERMS; ++q) terms_out[q] += tmp[q];
   }
   return KGS_OK;
+}
+
+int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap) {
+  if (N < 1 || C < 1 || nsteps < 0) return -1;
+  const std::vector<PipeEvent> plan = pipeline_plan(N, C, pipeline_shrinks(nsteps));
+  const int64_t n = (int64_t)plan.size();
+  for (int64_t i = 0; i < std::min(n, cap); ++i) {
+    out[4 * i] = plan[i].kind;
+    out[4 * i + 1] = plan[i].pass;
+    out[4 * i + 2] = plan[i].a;
+    out[4 * i + 3] = plan[i].b;
+  }
+  return n;
 }
 
 int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
