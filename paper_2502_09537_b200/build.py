@@ -18,7 +18,7 @@ REPO = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libkgs_b200.so"
 SOURCES = [CSRC / "kgs_host.cu"]
-DEPS = SOURCES + [CSRC / "kgs_device.cuh", REPO / "include" / "kgs_b200.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [REPO / "include" / "kgs_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

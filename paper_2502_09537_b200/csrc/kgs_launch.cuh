@@ -1,0 +1,493 @@
+// kgs_launch.cuh -- kernel dispatch: simple and marching colour passes (TMA descriptors, tile variants), resident small-grid steps, fused ping-pong steps.
+// Part of the single translation unit kgs_host.cu (included in order).
+#pragma once
+
+namespace {
+
+// ---- kernel dispatch -----------------------------------------------------
+template <int D, int COL, int OP1, int OP2, bool DIAG, bool CHECK>
+int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
+             int step_no) {
+  auto kern = colour_pass<D, COL, OP1, OP2, DIAG, CHECK>;
+  static int occ = 0;  // per instantiation; all devices are B200
+  if (occ == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+    if (occ < 1) occ = 1;
+  }
+  const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
+  int64_t grid = std::min<int64_t>(g.ntiles, (int64_t)bps * ctx->nsm);
+  grid = std::min<int64_t>(grid, ctx->grid_cap);
+  if (grid < 1) return KGS_OK;  // nothing to do
+  kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(
+      g, c, s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no);
+  ctx->launches++;
+  if (DIAG) s.npart[COL] += (int)grid;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+// ---- TMA descriptors ------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 3-D march kernel variants: tile rows x slots, ring depths, min blocks/SM.
+// Larger tile cross-sections re-read fewer halo rows/slots.
+template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_, int CL_ = 1>
+struct MarchVariant {
+  static constexpr int TY = TY_, TK = TK_, NOTH = NOTH_, NOWN = NOWN_, MINB = MINB_, CL = CL_;
+  static constexpr int NT = TY * TK;
+  using L = MarchSmem<TY, TK, NOTH, NOWN>;
+};
+using MV0 = MarchVariant<4, 64, 4, 2, 4>;     // 256 threads, 4 blocks/SM
+using MV1 = MarchVariant<8, 64, 4, 2, 2>;     // 512 threads, 2 blocks/SM
+using MV2 = MarchVariant<16, 32, 4, 2, 2>;    // 512 threads, 2 blocks/SM
+using MV3 = MarchVariant<32, 32, 4, 2, 1>;    // 1024 threads, 1 block/SM
+using MV4 = MarchVariant<4, 64, 4, 2, 4, 8>;  // MV0 in clusters of 8 along y
+using MV5 = MarchVariant<4, 64, 4, 2, 4, 4>;  // MV0 in clusters of 4 along y
+constexpr int kMarchVariants = 6;
+constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY, MV4::TY, MV5::TY};
+constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK, MV4::TK, MV5::TK};
+constexpr int kVarCL[kMarchVariants] = {MV0::CL, MV1::CL, MV2::CL, MV3::CL, MV4::CL, MV5::CL};
+
+// L2 sector promotion of the TMA boxes.  The two-slot halo columns are 16 B
+// inside a neighbouring tile's lines: promoting them to 256-B fetches would
+// pull whole blocks of that tile from HBM.
+CUtensorMapL2promotion promo(int v) {
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
+// 4-D view of one colour array with dims ordered (slot, field, row, plane)
+// -- strides 8, pp*8, nk*8, ps*8 bytes -- so that a box lands in shared
+// memory as [row][field][slot] (MarchSmem); per variant four box shapes.
+int make_maps_for(kgs_ctx* ctx, Slab& s, double* const bufs[2], MarchMaps (&maps)[6][2]) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)ctx->nk, 4, (cuuint64_t)ctx->ny,
+                              (cuuint64_t)(s.nx + 2)};
+  const cuuint64_t strides[3] = {(cuuint64_t)ctx->pp * 8, (cuuint64_t)ctx->rs * 8,
+                                 (cuuint64_t)ctx->ps * 8};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  for (int v = 0; v < kMarchVariants; ++v) {
+    const int ty = kVarTY[v], tk = kVarTK[v];
+    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % (ty * kVarCL[v]) == 0 && ctx->nk % tk == 0 &&
+                     ctx->nk >= 2 && (ctx->rs * 8) % 16 == 0;
+    if (!s.has_tmaps[v]) continue;
+    const cuuint32_t centre[4] = {(cuuint32_t)tk, 3, (cuuint32_t)ty, 1};
+    const cuuint32_t row[4] = {(cuuint32_t)tk, 3, 1, 1};
+    const cuuint32_t col[4] = {2, 3, (cuuint32_t)ty, 1};
+    const cuuint32_t own[4] = {(cuuint32_t)tk, 4, (cuuint32_t)ty, 1};
+    for (int c = 0; c < 2; ++c) {
+      MarchMaps& m = maps[v][c];
+      CUtensorMap* outs[4] = {&m.centre, &m.row, &m.col, &m.own};
+      const cuuint32_t* boxes[4] = {centre, row, col, own};
+      for (int i = 0; i < 4; ++i) {
+        CUresult r = enc(outs[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[c], dims, strides,
+                         boxes[i], es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         promo(i == 3 ? ctx->tune_promo_tile : ctx->tune_promo_halo),
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+          return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled(variant %d, box %d) failed: %d", v,
+                      i, (int)r);
+      }
+    }
+  }
+  return KGS_OK;
+}
+
+// fused step: red pieces of one buffer set (StepSmem layout)
+constexpr int kStepTY = 16, kStepTK = 32;
+using StepS = StepSmem<kStepTY, kStepTK>;
+
+int make_step_maps(kgs_ctx* ctx, const Slab& s, double* red, StepMaps& m) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)ctx->nk, 4, (cuuint64_t)ctx->ny,
+                              (cuuint64_t)(s.nx + 2)};
+  const cuuint64_t strides[3] = {(cuuint64_t)ctx->pp * 8, (cuuint64_t)ctx->rs * 8,
+                                 (cuuint64_t)ctx->ps * 8};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const cuuint32_t centre[4] = {kStepTK, 3, kStepTY, 1};
+  const cuuint32_t rows2[4] = {kStepTK, 3, 2, 1};
+  const cuuint32_t col[4] = {2, 3, kStepTY, 1};
+  const cuuint32_t corner[4] = {2, 3, 1, 1};
+  CUtensorMap* outs[4] = {&m.centre, &m.rows2, &m.col, &m.corner};
+  const cuuint32_t* boxes[4] = {centre, rows2, col, corner};
+  for (int i = 0; i < 4; ++i) {
+    CUresult r = enc(outs[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, red, dims, strides, boxes[i],
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     promo(ctx->tune_promo_halo), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled(step box %d) failed: %d", i, (int)r);
+  }
+  return KGS_OK;
+}
+
+int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
+  int r = make_maps_for(ctx, s, s.buf, s.maps);
+  if (!r && s.alt[0]) r = make_maps_for(ctx, s, s.alt, s.amaps);
+  s.has_smap = false;
+  if (!r && s.alt[0] && ctx->ny % kStepTY == 0 && ctx->nk % kStepTK == 0) {
+    r = make_step_maps(ctx, s, s.buf[1], s.smap[0]);
+    if (!r) r = make_step_maps(ctx, s, s.alt[1], s.smap[1]);
+    if (!r) s.has_smap = true;
+  }
+  return r;
+}
+
+template <typename Var, int COL, int OP1, int OP2, bool DIAG, bool CHECK, int DBG = 0>
+int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
+                 int v) {
+  using L = typename Var::L;
+  constexpr int CL = Var::CL;
+  auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
+                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG, CL>;
+  static int occ = 0;  // resident CTAs per SM (or clusters per GPU / nsm when CL > 1)
+  static int max_clusters = 0;
+  if (occ == 0) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Var::NT, L::bytes));
+    if (occ < 1) return fail(ctx, KGS_ECUDA, "march kernel does not fit on an SM");
+    if (CL > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(CL * 64);
+      cfg.blockDim = dim3(Var::NT);
+      cfg.dynamicSmemBytes = L::bytes;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+      if (max_clusters < 1) return fail(ctx, KGS_ECUDA, "march cluster does not fit");
+    }
+  }
+  const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
+  int64_t G = std::min<int64_t>((int64_t)bps * ctx->nsm, ctx->grid_cap);
+  if (CL > 1) G = std::min<int64_t>(G, (int64_t)max_clusters * CL) / CL * CL;
+  const int64_t cols = (int64_t)(g.ny / Var::TY) * (g.nk / Var::TK);
+  const int nxr = g.xb - g.xa;
+  MarchCfg mc;
+  if (ctx->tune_xc > 0) mc.xc = std::min(ctx->tune_xc, nxr);
+  else  // ~8 units per resident block for load balance, >= 8 planes per unit
+    mc.xc = (int)std::max<int64_t>(std::min<int64_t>(nxr, 8),
+                                   std::min<int64_t>(nxr, (int64_t)nxr * cols / (8 * G)));
+  mc.nunits = (int64_t)((nxr + mc.xc - 1) / mc.xc) * cols;
+  mc.sync = std::max(1, ctx->tune_sync);
+  const int64_t grid = std::min<int64_t>(mc.nunits, G) / CL * CL;
+  if (grid < 1) return KGS_OK;
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(Var::NT);
+    cfg.dynamicSmemBytes = L::bytes;
+    cfg.stream = s.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, s.maps[v][COL ^ 1], s.maps[v][COL], g, c,
+                          s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no,
+                          mc));
+  } else {
+    kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
+        s.maps[v][COL ^ 1], s.maps[v][COL], g, c,
+        s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no, mc);
+  }
+  ctx->launches++;
+  if (DIAG) s.npart[COL] += (int)grid;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+// ---- resident steps (whole state in one CTA's shared memory) -------------
+constexpr size_t kResidentMaxBytes = 200 * 1024;
+
+bool resident_eligible(const kgs_ctx* ctx) {
+  if (!ctx->tune_resident || ctx->slabs.size() != 1 || (ctx->dist && ctx->nranks > 1))
+    return false;
+  const Slab& s = ctx->slabs[0];
+  return (size_t)s.nx * ctx->ps * 2 * sizeof(double) <= kResidentMaxBytes;
+}
+
+template <int D>
+int launch_resident_d(kgs_ctx* ctx, Slab& s, const Coeffs& c, const ResidentCfg& rc) {
+  auto kern = resident_steps<D>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kResidentMaxBytes));
+    attr = true;
+  }
+  PassGeom gb = make_geom(ctx, s, 0, 0, s.nx), gr = make_geom(ctx, s, 1, 0, s.nx);
+  const size_t bytes = (size_t)s.nx * ctx->ps * 2 * sizeof(double);
+  kern<<<1, 1024, bytes, s.stream>>>(gb, gr, c, rc, s.records, s.bad);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+int launch_resident(kgs_ctx* ctx, const Coeffs& c, int64_t nsteps, int64_t step_offset,
+                    int64_t record_stride, bool head_fused, bool defer) {
+  Slab& s = ctx->slabs[0];
+  CK(cudaSetDevice(s.dev));
+  ResidentCfg rc;
+  rc.nsteps = nsteps;
+  rc.step_offset = step_offset;
+  rc.record_stride = record_stride;
+  rc.head_fused = head_fused ? 1 : 0;
+  rc.defer = defer ? 1 : 0;
+  switch (ctx->d) {
+    case 1: return launch_resident_d<1>(ctx, s, c, rc);
+    case 2: return launch_resident_d<2>(ctx, s, c, rc);
+    default: return launch_resident_d<3>(ctx, s, c, rc);
+  }
+}
+
+// ---- fused steps (ping-pong buffer sets) ---------------------------------
+bool needs_exchange(const kgs_ctx* ctx);
+int exchange(kgs_ctx* ctx, int col);
+
+// Geometry-only test (no allocation): 3-D, tiles divide the planes, and a
+// multi-slab run leaves interior K4 planes [1, nx-1).
+bool fused_geometry(const kgs_ctx* ctx) {
+  if (!ctx->tune_fused || ctx->alt_failed || ctx->d != 3 || ctx->tune_xc < 0) return false;
+  if (ctx->ny % kStepTY || ctx->nk % kStepTK) return false;
+  for (auto& s : ctx->slabs)
+    if (s.nx < 4) return false;
+  return true;
+}
+
+// Allocate the second buffer set on first use; if it does not fit, run
+// two-pass steps from then on (same results, more traffic).
+bool fused_ready(kgs_ctx* ctx) {
+  if (!fused_geometry(ctx)) return false;
+  for (auto& s : ctx->slabs) {
+    if (s.alt[0] && s.has_smap) continue;
+    if (cudaSetDevice(s.dev) != cudaSuccess) return false;
+    const size_t colour_bytes = (size_t)(s.nx + 2) * ctx->ps * sizeof(double);
+    for (int c = 0; c < 2 && !ctx->alt_failed; ++c) {
+      if (s.alt[c]) continue;
+      if (cudaMalloc(&s.alt[c], colour_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        s.alt[c] = nullptr;
+        ctx->alt_failed = true;
+      } else {
+        s.alt0[c] = s.alt[c] + ctx->ps;
+      }
+    }
+    if (ctx->alt_failed || make_tensor_maps(ctx, s) || !s.has_smap) {
+      for (auto& t : ctx->slabs)
+        for (int c = 0; c < 2; ++c) {
+          if (t.alt[c]) cudaFree(t.alt[c]);
+          t.alt[c] = t.alt0[c] = nullptr;
+        }
+      ctx->alt_failed = true;
+      return false;
+    }
+  }
+  return true;
+}
+
+void swap_sets(kgs_ctx* ctx) {
+  for (auto& s : ctx->slabs) {
+    for (int c = 0; c < 2; ++c) {
+      std::swap(s.buf[c], s.alt[c]);
+      std::swap(s.plane0[c], s.alt0[c]);
+    }
+    std::swap(s.maps, s.amaps);
+    std::swap(s.smap[0], s.smap[1]);
+  }
+}
+
+template <bool DIAG, int K4OP2>
+int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int xb) {
+  constexpr int NT = kStepTY * kStepTK;
+  auto kern = step_pass<DIAG, K4OP2, kStepTY, kStepTK, 2>;
+  static int occ = 0;
+  if (occ == 0) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)StepS::bytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, StepS::bytes));
+    if (occ < 1) return fail(ctx, KGS_ECUDA, "fused step kernel does not fit on an SM");
+  }
+  StepGeom g{};
+  g.rold = s.plane0[1];
+  g.bold = s.plane0[0];
+  g.rnew = s.alt0[1];
+  g.bnew = s.alt0[0];
+  g.ps = ctx->ps;
+  g.pp = ctx->pp;
+  g.rs = ctx->rs;
+  g.nx = s.nx;
+  g.ny = ctx->ny;
+  g.nk = ctx->nk;
+  g.x0 = s.x0;
+  g.wrap = needs_exchange(ctx) ? 0 : 1;
+  g.xa = xa;
+  g.xb = xb;
+  g.wa = 0;
+  g.wb = s.nx;
+  g.xc = std::max(1, std::min(ctx->tune_fused_xc, xb - xa));
+  g.dbg = ctx->tune_fused_dbg;
+  const int64_t ncols = (int64_t)(ctx->ny / kStepTY) * (ctx->nk / kStepTK);
+  g.nunits = (int64_t)((xb - xa + g.xc - 1) / g.xc) * ncols;
+  const int64_t grid = std::min<int64_t>({g.nunits, (int64_t)occ * ctx->nsm, ctx->grid_cap});
+  kern<<<(unsigned)grid, NT, StepS::bytes, s.stream>>>(
+      s.smap[0], g, c, s.partials[1] + (int64_t)s.npart[1] * NTERMS, s.bad, step_no);
+  ctx->launches++;
+  if (DIAG) s.npart[1] += (int)grid;
+  CK(cudaGetLastError());
+  return KGS_OK;
+}
+
+int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
+                bool check, const Coeffs& c, int step_no, int xa, int xb,
+                const double* own_in, double* mir_lo, double* mir_hi);
+
+// One DP-AVF2 step n as a fused march (K3(n) then K4(n), or the red adjoint
+// tail when `last`), step-n state in the current set, result in the other;
+// the sets are swapped after the launch.  Several slabs: the march does K4
+// on planes [1, nx-1) only; the black faces are exchanged and K4 on planes
+// 0 and nx-1 runs as a small pass reading the old red (own_in) and the new
+// black ghosts, writing the new red; then the red faces are exchanged.
+int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) {
+  const bool multi = needs_exchange(ctx);
+  ctx->mirrored[0] = ctx->mirrored[1] = false;  // this path exchanges by copies
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    if (s.xch_pending) {   // red ghosts of the current set (K3 at planes 0, nx-1)
+      CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+      s.xch_pending = false;
+    }
+    if (rec) { s.npart[1] = 0; s.npart[0] = 0; }
+    const int xa = multi ? 1 : 0, xb = multi ? s.nx - 1 : s.nx;
+    int r;
+    if (rec) r = last ? launch_step<true, OP_NONE>(ctx, s, c, step_no, xa, xb)
+                      : launch_step<true, OP_BASE>(ctx, s, c, step_no, xa, xb);
+    else     r = last ? launch_step<false, OP_NONE>(ctx, s, c, step_no, xa, xb)
+                      : launch_step<false, OP_BASE>(ctx, s, c, step_no, xa, xb);
+    if (r) return r;
+  }
+  swap_sets(ctx);
+  if (!multi) return KGS_OK;
+  int r = exchange(ctx, 0);
+  const int op2 = last ? OP_NONE : OP_BASE;
+  for (auto& s : ctx->slabs) {
+    if (r) return r;
+    CK(cudaSetDevice(s.dev));
+    if (s.xch_pending) {
+      CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+      s.xch_pending = false;
+    }
+    r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, 0, 1, s.alt0[1], nullptr,
+                    nullptr);
+    if (!r) r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, s.nx - 1, s.nx,
+                            s.alt0[1], nullptr, nullptr);
+  }
+  if (!r) r = exchange(ctx, 1);
+  return r;
+}
+
+// march variant to use for this pass, or -1 for the simple kernel
+int march_variant(const kgs_ctx* ctx, const Slab& s, const PassGeom& g) {
+  if (ctx->d != 3 || ctx->tune_xc < 0 || g.xb - g.xa < 1) return -1;
+  if (g.own != g.own_out) return -1;  // reads another buffer: simple kernel
+  int v = ctx->tune_variant;
+  if (v >= 0 && v < kMarchVariants && s.has_tmaps[v]) return v;
+  for (v = 0; v < kMarchVariants; ++v)   // fall back to any eligible variant
+    if (s.has_tmaps[v]) return v;
+  return -1;
+}
+
+template <int COL, int O1, int O2, bool DG, bool CH>
+int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
+                     int v) {
+  switch (v) {
+    case 0: return launch_march<MV0, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 1: return launch_march<MV1, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 2: return launch_march<MV2, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 3: return launch_march<MV3, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 4: return launch_march<MV4, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    default: return launch_march<MV5, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+  }
+}
+
+template <int D, int COL>
+int launch_col(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
+               int op1, int op2, bool diag, bool check, int step_no) {
+#define KGS_CASE(O1, O2, DG, CH)                                          \
+  if (op1 == O1 && op2 == O2 && diag == DG && check == CH) {             \
+    if (D == 3) {                                                        \
+      const int v_ = march_variant(ctx, s, g);                           \
+      if (v_ >= 0)                                                       \
+        return launch_march_any<COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v_); \
+    }                                                                    \
+    return launch_t<D, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no);      \
+  }
+  // single sweeps (kgs_sweep, head)
+  KGS_CASE(OP_BASE, OP_NONE, false, false)
+  KGS_CASE(OP_ADJ, OP_NONE, false, false)
+  // diagnostics / finiteness only
+  KGS_CASE(OP_NONE, OP_NONE, true, false)
+  KGS_CASE(OP_NONE, OP_NONE, false, true)
+  if (COL == 0) {  // K3: black base(n) + adjoint(n)
+    KGS_CASE(OP_BASE, OP_ADJ, false, true)
+    KGS_CASE(OP_BASE, OP_ADJ, true, true)
+  } else {  // K4: red adjoint(n) + base(n+1); tail: red adjoint(n)
+    KGS_CASE(OP_ADJ, OP_BASE, false, false)   // deferred tail fused into a head
+    KGS_CASE(OP_ADJ, OP_BASE, false, true)
+    KGS_CASE(OP_ADJ, OP_BASE, true, true)
+    KGS_CASE(OP_ADJ, OP_NONE, false, true)
+    KGS_CASE(OP_ADJ, OP_NONE, true, true)
+  }
+#undef KGS_CASE
+  return fail(ctx, KGS_EINVAL, "unsupported pass combination %d/%d/%d/%d",
+              op1, op2, (int)diag, (int)check);
+}
+
+// own_in: read this colour from another buffer (same geometry) and write
+// the result to the current one; uses the simple kernel.
+int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
+                bool check, const Coeffs& c, int step_no, int xa = 0, int xb = -1,
+                const double* own_in = nullptr, double* mir_lo = nullptr,
+                double* mir_hi = nullptr) {
+  PassGeom g = make_geom(ctx, s, col, xa, xb < 0 ? s.nx : xb);
+  if (own_in) g.own = const_cast<double*>(own_in);
+  g.mir_lo = mir_lo;
+  g.mir_hi = mir_hi;
+  switch (ctx->d * 2 + col) {
+    case 2: return launch_col<1, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 3: return launch_col<1, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 4: return launch_col<2, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 5: return launch_col<2, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 6: return launch_col<3, 0>(ctx, s, g, c, op1, op2, diag, check, step_no);
+    case 7: return launch_col<3, 1>(ctx, s, g, c, op1, op2, diag, check, step_no);
+  }
+  return fail(ctx, KGS_EINVAL, "bad dimension %d", ctx->d);
+}
+
+}  // namespace

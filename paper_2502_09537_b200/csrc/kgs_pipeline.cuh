@@ -1,0 +1,291 @@
+// kgs_pipeline.cuh -- pipelined host integration (kgs_integrate_host): the wavefront plan and its execution.
+// Part of the single translation unit kgs_host.cu (included in order).
+#pragma once
+
+namespace {
+
+// ---- pipelined host integration (kgs_integrate_host) ---------------------
+// Upload, the colour passes of a whole integrate() call and the download
+// overlap.  Chunks of C planes arrive in folded order (block 0, the last
+// block, block 1, the one before, ...), so the arrived region is a periodic
+// interval around plane 0 that grows on alternating sides.  Every pass reads
+// the other colour at x-1..x+1 and overwrites what its predecessor read, so
+// pass j may cover its predecessor's done region shrunk by one plane on each
+// side (RAW and WAR at once); the whole ring once the predecessor has it.
+// All passes therefore advance as a wavefront behind the upload, on the
+// compute stream in dependency order, and a C-plane block is downloaded
+// (merge kernel + D2H on a third stream) as soon as the last pass covered it:
+// H2D, compute and D2H proceed together (PCIe is full duplex).  The initial
+// state is also copied device-side (the second buffer set) so a non-finite
+// step can be replayed exactly.  Records get their own partial regions (the
+// DIAG passes of different steps are in flight together).
+int ensure_alt(kgs_ctx* ctx) {
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    const size_t colour_bytes = (size_t)(s.nx + 2) * ctx->ps * sizeof(double);
+    for (int c = 0; c < 2; ++c) {
+      if (s.alt[c]) continue;
+      if (cudaMalloc(&s.alt[c], colour_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        s.alt[c] = nullptr;
+        return KGS_ENOMEM;
+      }
+      s.alt0[c] = s.alt[c] + ctx->ps;
+    }
+  }
+  return KGS_OK;
+}
+
+struct PipePass {
+  int col, op1, op2;
+  bool diag, check;
+  int step_no;
+  int rec;      // record of its DIAG partials (-1: none)
+  int shrink;   // planes given up on each side relative to the predecessor
+};
+
+constexpr int kPipeFallback = 1;   // not eligible / no memory: use the plain path
+
+// The pipeline as a list of events, in the order they are issued on the
+// compute stream: ARRIVE (wait for chunk m = planes [a, b)), PASS (pass j
+// over planes [a, b)), FINAL (planes [a, b) are final: copy them back).
+// Pure host logic (kgs_pipeline_plan exports it for the CPU tests).
+enum PipeKind : int { PIPE_ARRIVE = 0, PIPE_PASS = 1, PIPE_FINAL = 2 };
+struct PipeEvent {
+  int kind, pass;
+  int64_t a, b;
+};
+
+std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int>& shrink) {
+  std::vector<PipeEvent> ev;
+  const int64_t nb = (N + C - 1) / C;
+  const int J = (int)shrink.size();
+  std::vector<int64_t> lo(J, 0), hi(J, 0);   // done regions, unwrapped: empty or lo < hi
+  std::vector<char> full(J, 0), dl(nb, 0);
+  auto pass = [&](int j, int64_t a, int64_t b) {
+    if (b > a) ev.push_back({PIPE_PASS, j, a, b});
+  };
+  auto pass_u = [&](int j, int64_t u0, int64_t u1) {   // unwrapped range, u1 - u0 <= N
+    if (u1 <= u0) return;
+    while (u0 < 0) { u0 += N; u1 += N; }
+    while (u0 >= N) { u0 -= N; u1 -= N; }
+    if (u1 <= N) pass(j, u0, u1);
+    else { pass(j, u0, N); pass(j, 0, u1 - N); }
+  };
+  int64_t alo = 0, ahi = 0;
+  for (int64_t m = 0; m < nb; ++m) {
+    const int64_t blk = (m % 2 == 0) ? m / 2 : nb - 1 - m / 2;   // folded order
+    const int64_t x0 = blk * C, x1 = std::min(N, x0 + C);
+    ev.push_back({PIPE_ARRIVE, (int)m, x0, x1});
+    if (m % 2 == 0) ahi = x1; else alo = x0 - N;
+    int64_t plo = alo, phi = ahi;
+    bool pfull = m == nb - 1;
+    for (int j = 0; j < J; ++j) {
+      if (!full[j]) {
+        if (pfull) {   // the rest of the ring; the region need not contain plane 0
+          if (lo[j] == hi[j]) pass(j, 0, N);
+          else pass_u(j, hi[j], lo[j] + N);
+          full[j] = 1;
+        } else {
+          const int64_t nlo = plo + shrink[j], nhi = phi - shrink[j];
+          if (nhi > nlo) {
+            if (lo[j] == hi[j]) pass_u(j, nlo, nhi);
+            else { pass_u(j, nlo, lo[j]); pass_u(j, hi[j], nhi); }
+            lo[j] = nlo;
+            hi[j] = nhi;
+          }
+        }
+      }
+      pfull = full[j];
+      plo = lo[j];
+      phi = hi[j];
+    }
+    // blocks wholly inside the last pass's done region (which need not
+    // contain plane 0 yet) are final
+    const int64_t L = lo[J - 1], H = hi[J - 1];
+    for (int64_t k = 0; k < nb; ++k) {
+      if (dl[k]) continue;
+      const int64_t b0 = k * C, b1 = std::min(N, b0 + C);
+      if (full[J - 1] || (L < H && ((b0 >= L && b1 <= H) || (b0 - N >= L && b1 - N <= H)))) {
+        dl[k] = 1;
+        ev.push_back({PIPE_FINAL, (int)k, b0, b1});
+      }
+    }
+  }
+  return ev;
+}
+
+std::vector<int> pipeline_shrinks(int64_t nsteps) {
+  // initial energy (black self, red edges + self), head, then K3/K4 per step
+  std::vector<int> sh = {0, 1, 0};
+  for (int64_t i = 0; i < 2 * nsteps; ++i) sh.push_back(1);
+  return sh;
+}
+
+int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, int64_t nsteps,
+                        int64_t step_offset, int64_t record_stride, int64_t nrec,
+                        unsigned long long* bad_out) {
+  if (!ctx->tune_pipe || ctx->slabs.size() != 1 || ctx->dist || ctx->d != 3)
+    return kPipeFallback;
+  Slab& s = ctx->slabs[0];
+  const int64_t N = s.nx;
+  const int64_t C = std::max<int64_t>(1, ctx->tune_pipe_chunk);
+  const int64_t nb = (N + C - 1) / C;
+  if (nb < 4) return kPipeFallback;
+  const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
+  CK(cudaSetDevice(s.dev));
+  if (ensure_alt(ctx)) return kPipeFallback;
+  const int64_t stage = 4 * C * nat_plane;
+  if (s.pipe_stage < stage) {
+    if (s.pipe_up) CK(cudaFree(s.pipe_up));
+    if (s.pipe_dn) CK(cudaFree(s.pipe_dn));
+    s.pipe_up = s.pipe_dn = nullptr;
+    s.pipe_stage = 0;
+    if (cudaMalloc(&s.pipe_up, stage * 8) != cudaSuccess ||
+        cudaMalloc(&s.pipe_dn, stage * 8) != cudaSuccess) {
+      cudaGetLastError();
+      if (s.pipe_up) cudaFree(s.pipe_up);
+      s.pipe_up = nullptr;
+      return kPipeFallback;
+    }
+    s.pipe_stage = stage;
+  }
+  const int64_t maxl = nb + 4;                                 // launches per pass
+  const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
+  const int64_t need = (nrec + 1) * 2 * region;
+  if (s.pipe_part_cap < need) {
+    if (need > (int64_t)1 << 27) return kPipeFallback;         // > 1 GiB of partials
+    if (s.pipe_part) CK(cudaFree(s.pipe_part));
+    s.pipe_part = nullptr;
+    s.pipe_part_cap = 0;
+    if (cudaMalloc(&s.pipe_part, need * 8) != cudaSuccess) {
+      cudaGetLastError();
+      return kPipeFallback;
+    }
+    s.pipe_part_cap = need;
+  }
+  if (!s.dstream) CK(cudaStreamCreateWithFlags(&s.dstream, cudaStreamNonBlocking));
+  while ((int64_t)s.pipe_ev.size() < 2 * nb) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s.pipe_ev.push_back(e);
+  }
+  int r = ensure_records(ctx, nrec + 1);
+  if (!r) r = reset_bad(ctx);
+  if (r) return r;
+  ctx->pending = false;   // the whole state is replaced
+
+  // the passes of the call: initial energy (black self, red edges + self),
+  // head, then K3(n), K4(n) per step (K4 of the last step = the tail)
+  std::vector<PipePass> passes;
+  passes.push_back({0, OP_NONE, OP_NONE, true, false, 0, 0, 0});
+  passes.push_back({1, OP_NONE, OP_NONE, true, false, 0, 0, 1});
+  passes.push_back({1, OP_BASE, OP_NONE, false, false, 0, -1, 0});
+  int64_t slot = 0;
+  for (int64_t i = 1; i <= nsteps; ++i) {
+    const int64_t n = step_offset + i;
+    const bool rec = record_stride > 0 && n % record_stride == 0;
+    const int rid = rec ? (int)(1 + slot++) : -1;
+    passes.push_back({0, OP_BASE, OP_ADJ, rec, true, (int)n, rid, 1});
+    passes.push_back({1, OP_ADJ, i < nsteps ? OP_BASE : OP_NONE, rec, true, (int)n, rid, 1});
+  }
+  const int J = (int)passes.size();
+  std::vector<int64_t> roff((size_t)(nrec + 1) * 2, 0);
+  std::vector<int> shrink(J);
+  for (int j = 0; j < J; ++j) shrink[j] = passes[j].shrink;
+  const std::vector<PipeEvent> plan = pipeline_plan(N, C, shrink);
+
+  auto launch_range = [&](const PipePass& P, int64_t xa, int64_t xb) -> int {
+    if (xb <= xa) return KGS_OK;
+    double* save = s.partials[P.col];
+    const int64_t ri = P.diag ? (int64_t)P.rec * 2 + P.col : 0;
+    if (P.diag) {
+      s.partials[P.col] = s.pipe_part + ri * region;
+      s.npart[P.col] = (int)roff[ri];
+    }
+    int rr = launch_pass(ctx, s, P.col, P.op1, P.op2, P.diag, P.check, c, P.step_no, (int)xa,
+                         (int)xb);
+    if (P.diag) {
+      roff[ri] = s.npart[P.col];
+      s.partials[P.col] = save;
+    }
+    return rr;
+  };
+
+  CK(cudaEventRecord(s.ev_t0, s.cstream));
+  // uploads (folded block order) on the comm stream: H2D, split, backup copy
+  for (const PipeEvent& e : plan) {
+    if (e.kind != PIPE_ARRIVE) continue;
+    const int64_t m = e.pass, x0 = e.a, x1 = e.b, nxc = x1 - x0;
+    for (int f = 0; f < 4; ++f)
+      CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + x0 * nat_plane,
+                         (size_t)nxc * nat_plane * 8, cudaMemcpyHostToDevice, s.cstream));
+    const int64_t cnt = nxc * ctx->ny * ctx->nk;
+    const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
+    for (int f = 0; f < 4; ++f) {
+      PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
+      g.own += f * ctx->pp;
+      g.oth += f * ctx->pp;
+      split_field<<<blocks, 256, 0, s.cstream>>>(s.pipe_up + f * C * nat_plane, g, (int)nxc,
+                                                  (int)x0);
+      ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    for (int cc = 0; cc < 2; ++cc)
+      CK(cudaMemcpyAsync(s.alt0[cc] + x0 * ctx->ps, s.plane0[cc] + x0 * ctx->ps,
+                         (size_t)nxc * ctx->ps * 8, cudaMemcpyDeviceToDevice, s.cstream));
+    CK(cudaEventRecord(s.pipe_ev[m], s.cstream));
+  }
+
+  // the wavefront on the compute stream; downloads behind it
+  int64_t ndl = 0;
+  for (const PipeEvent& e : plan) {
+    if (r) break;
+    if (e.kind == PIPE_ARRIVE) {
+      CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[e.pass], 0));
+    } else if (e.kind == PIPE_PASS) {
+      r = launch_range(passes[e.pass], e.a, e.b);
+    } else {
+      const int64_t k = e.pass, b0 = e.a, nxc = e.b - e.a;
+      ++ndl;
+      cudaEvent_t ev = s.pipe_ev[nb + k];
+      CK(cudaEventRecord(ev, s.stream));
+      CK(cudaStreamWaitEvent(s.dstream, ev, 0));
+      const int64_t cnt = nxc * ctx->ny * ctx->nk;
+      const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
+      for (int f = 0; f < 4; ++f) {
+        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
+        g.own += f * ctx->pp;
+        g.oth += f * ctx->pp;
+        merge_field<<<blocks, 256, 0, s.dstream>>>(s.pipe_dn + f * C * nat_plane, g, (int)nxc,
+                                                    (int)b0);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(host[f] + b0 * nat_plane, s.pipe_dn + f * C * nat_plane,
+                           (size_t)nxc * nat_plane * 8, cudaMemcpyDeviceToHost, s.dstream));
+      }
+      CK(cudaGetLastError());
+    }
+  }
+  if (r) return r;
+  if (ndl != nb) return fail(ctx, KGS_ECUDA, "pipeline copied back %lld of %lld blocks",
+                             (long long)ndl, (long long)nb);
+  for (int64_t q = 0; q <= nrec; ++q) {
+    finalize_terms<<<1, kThreads, 0, s.stream>>>(
+        s.pipe_part + (q * 2 + 1) * region, (int)roff[q * 2 + 1], s.pipe_part + (q * 2) * region,
+        (int)roff[q * 2], s.records + q * NTERMS);
+    ctx->launches++;
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s.ev_done, s.dstream));
+  CK(cudaStreamWaitEvent(s.stream, s.ev_done, 0));
+  CK(cudaEventRecord(s.ev_t1, s.stream));
+  r = sync_all(ctx);
+  if (!r) CK(cudaStreamSynchronize(s.dstream));
+  if (r) return r;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, s.ev_t0, s.ev_t1));
+  ctx->last_ms = ms;
+  return read_bad(ctx, bad_out);
+}
+
+}  // namespace
