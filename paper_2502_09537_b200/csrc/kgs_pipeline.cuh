@@ -61,7 +61,7 @@ std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int
   const int64_t nb = (N + C - 1) / C;
   const int J = (int)shrink.size();
   std::vector<int64_t> lo(J, 0), hi(J, 0);   // done regions, unwrapped: empty or lo < hi
-  std::vector<char> full(J, 0), dl(nb, 0);
+  std::vector<char> dl(nb, 0);
   auto pass = [&](int j, int64_t a, int64_t b) {
     if (b > a) ev.push_back({PIPE_PASS, j, a, b});
   };
@@ -72,20 +72,26 @@ std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int
     if (u1 <= N) pass(j, u0, u1);
     else { pass(j, u0, N); pass(j, 0, u1 - N); }
   };
-  int64_t alo = 0, ahi = 0;
-  for (int64_t m = 0; m < nb; ++m) {
-    const int64_t blk = (m % 2 == 0) ? m / 2 : nb - 1 - m / 2;   // folded order
-    const int64_t x0 = blk * C, x1 = std::min(N, x0 + C);
-    ev.push_back({PIPE_ARRIVE, (int)m, x0, x1});
-    if (m % 2 == 0) ahi = x1; else alo = x0 - N;
+  auto full = [&](int j) { return hi[j] - lo[j] >= N; };
+  // One round: every pass extends its done region as far as its predecessor
+  // allows -- the predecessor's region shrunk by `shrink` planes per side; once
+  // the predecessor has the whole ring, by at most C planes per side, so the
+  // last planes close from both edges inward and blocks near the edges
+  // become final (and go back) while the middle still computes.
+  auto round = [&](int64_t alo, int64_t ahi) {
     int64_t plo = alo, phi = ahi;
-    bool pfull = m == nb - 1;
     for (int j = 0; j < J; ++j) {
-      if (!full[j]) {
-        if (pfull) {   // the rest of the ring; the region need not contain plane 0
-          if (lo[j] == hi[j]) pass(j, 0, N);
-          else pass_u(j, hi[j], lo[j] + N);
-          full[j] = 1;
+      if (!full(j)) {
+        if (phi - plo >= N) {                   // predecessor complete
+          if (lo[j] == hi[j]) { pass(j, 0, N); lo[j] = 0; hi[j] = N; }
+          else {
+            const int64_t gap = N - (hi[j] - lo[j]);
+            const int64_t r = std::min(C, gap), l = std::min(C, gap - r);
+            pass_u(j, hi[j], hi[j] + r);
+            pass_u(j, lo[j] - l, lo[j]);
+            hi[j] += r;
+            lo[j] -= l;
+          }
         } else {
           const int64_t nlo = plo + shrink[j], nhi = phi - shrink[j];
           if (nhi > nlo) {
@@ -96,22 +102,31 @@ std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int
           }
         }
       }
-      pfull = full[j];
       plo = lo[j];
       phi = hi[j];
     }
     // blocks wholly inside the last pass's done region (which need not
-    // contain plane 0 yet) are final
+    // contain plane 0) are final
     const int64_t L = lo[J - 1], H = hi[J - 1];
     for (int64_t k = 0; k < nb; ++k) {
       if (dl[k]) continue;
       const int64_t b0 = k * C, b1 = std::min(N, b0 + C);
-      if (full[J - 1] || (L < H && ((b0 >= L && b1 <= H) || (b0 - N >= L && b1 - N <= H)))) {
+      if (full(J - 1) || (L < H && ((b0 >= L && b1 <= H) || (b0 - N >= L && b1 - N <= H)))) {
         dl[k] = 1;
         ev.push_back({PIPE_FINAL, (int)k, b0, b1});
       }
     }
+  };
+  int64_t alo = 0, ahi = 0;
+  for (int64_t m = 0; m < nb; ++m) {
+    const int64_t blk = (m % 2 == 0) ? m / 2 : nb - 1 - m / 2;   // folded order
+    const int64_t x0 = blk * C, x1 = std::min(N, x0 + C);
+    ev.push_back({PIPE_ARRIVE, (int)m, x0, x1});
+    if (m % 2 == 0) ahi = x1; else alo = x0 - N;
+    if (m == nb - 1) { alo = 0; ahi = N; }       // the whole ring has arrived
+    round(alo, ahi);
   }
+  for (int guard = 0; !full(J - 1) && guard < 4 * (int)nb + J + 4; ++guard) round(0, N);
   return ev;
 }
 
