@@ -1,4 +1,5 @@
-// kgs_pipeline.cuh -- pipelined host integration (kgs_integrate_host): the wavefront plan and its execution.
+// kgs_pipeline.cuh -- pipelined host integration (kgs_integrate_host):
+// the wavefront plan and its execution.
 // Part of the single translation unit kgs_host.cu (included in order).
 #pragma once
 
@@ -15,7 +16,11 @@ namespace {
 // All passes therefore advance as a wavefront behind the upload, on the
 // compute stream in dependency order, and a C-plane block is downloaded
 // (merge kernel + D2H on a third stream) as soon as the last pass covered it:
-// H2D, compute and D2H proceed together (PCIe is full duplex).  The initial
+// H2D, compute and D2H proceed together (pinned copies: 55-57 GB/s one way,
+// 46 GB/s each way when both run).  After the last chunk, a pass whose
+// predecessor has the whole ring grows by one chunk per side per round, so
+// the remaining gap closes from its edges and those blocks go back while the
+// middle still computes.  The initial
 // state is also copied device-side (the second buffer set) so a non-finite
 // step can be replayed exactly.  Records get their own partial regions (the
 // DIAG passes of different steps are in flight together).
