@@ -30,7 +30,7 @@ def _run(g, sc, s0, tau, T, stride, pipeline, planes=32):
 @pytest.mark.parametrize("N,steps,stride,planes", [
     (128, 5, 1, 32), (128, 7, 3, 8), (128, 4, 4, 5), (192, 3, 2, 16), (256, 6, 6, 32),
     (128, 1, 1, 32), (64, 9, 2, 4), (128, 1, 1, 3), (128, 2, 1, 6), (128, 3, 3, 7),
-    (128, 20, 5, 32)])
+    (128, 20, 5, 32), (512, 10, 5, 32)])
 def test_pipeline_bitwise_vs_plain_and_oracle(N, steps, stride, planes):
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(N)
