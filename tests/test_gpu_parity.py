@@ -6,6 +6,8 @@ from numpy's pairwise sums; SURVEY.md App.B measured ~1e-15 relative).
 """
 from __future__ import annotations
 
+import hashlib
+
 import numpy as np
 import pytest
 
@@ -212,6 +214,30 @@ def test_1024cubed_full_size_smoke():
     assert dev.is_finite()
     assert tr.max_rel_error() < 1e-11
     dev.close()
+
+
+def test_1024cubed_decomposition_invariance():
+    """At the benchmark size: one slab (x wraps in the kernel) and 8 virtual
+    slabs (fused halo stores between them) give the same bits.  After 3
+    steps (7 passes) a decomposition error could only reach 7 planes from a
+    slab boundary, so the planes within 8 of every boundary are compared."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(1024)
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    digests = []
+    for ex in (None, kgs.CudaExecutor((0,), slabs_per_device=8)):
+        dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g, ex)
+        dev.ctx.step_dpavf2(args, 3, 0, 0)
+        h = hashlib.sha256()
+        buf = np.empty(16 * g.N * g.N)
+        for f in range(4):
+            for b in range(0, g.N, g.N // 8):          # slab boundaries (incl. the wrap)
+                for x0 in ((b - 8) % g.N, b):
+                    dev.ctx.download_planes(f, x0, buf[: 8 * g.N * g.N])
+                    h.update(buf[: 8 * g.N * g.N].tobytes())
+        digests.append(h.hexdigest())
+        dev.close()
+    assert digests[0] == digests[1]
 
 
 def test_shared_reciprocal_division():
