@@ -377,11 +377,24 @@ int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
 int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) {
   const bool multi = needs_exchange(ctx);
   ctx->mirrored[0] = ctx->mirrored[1] = false;  // this path exchanges by copies
-  for (auto& s : ctx->slabs) {
+  // With fused halo stores this step takes part in their event protocol as
+  // one pass k: the ghosts it reads may have been stored by the neighbours'
+  // previous pass (wait for their ev_face of k-1), and a later storing pass
+  // must wait until this step stopped reading ghosts (ev_face of k below).
+  const bool mirror = multi && ctx->mirror && ctx->tune_mirror;
+  const int64_t k = ctx->pass_no;
+  if (multi) ctx->pass_no++;
+  const int ns = (int)ctx->slabs.size();
+  for (int i = 0; i < ns; ++i) {
+    Slab& s = ctx->slabs[i];
     CK(cudaSetDevice(s.dev));
     if (s.xch_pending) {   // red ghosts of the current set (K3 at planes 0, nx-1)
       CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
       s.xch_pending = false;
+    }
+    if (mirror && k > 0) {
+      CK(cudaStreamWaitEvent(s.stream, ctx->slabs[(i - 1 + ns) % ns].ev_face[(k - 1) & 1], 0));
+      CK(cudaStreamWaitEvent(s.stream, ctx->slabs[(i + 1) % ns].ev_face[(k - 1) & 1], 0));
     }
     if (rec) { s.npart[1] = 0; s.npart[0] = 0; }
     const int xa = multi ? 1 : 0, xb = multi ? s.nx - 1 : s.nx;
@@ -407,6 +420,7 @@ int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) 
                     nullptr);
     if (!r) r = launch_pass(ctx, s, 1, OP_ADJ, op2, rec, true, c, step_no, s.nx - 1, s.nx,
                             s.alt0[1], nullptr, nullptr);
+    if (!r && mirror) CK(cudaEventRecord(s.ev_face[k & 1], s.stream));
   }
   if (!r) r = exchange(ctx, 1);
   return r;

@@ -1,0 +1,82 @@
+"""Randomised equivalence of the execution paths added for performance
+(hypothesis): the pipelined host integration (any chunk size, step count,
+record stride, with or without a non-finite value), and the multi-slab
+variants (fused halo stores vs copies, fused one-march steps vs two passes)
+-- all bitwise the plain path's fields, same records up to summation order,
+same first bad step."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+import paper_2502_09537_b200 as kgs
+from conftest import assert_bitwise
+from paper_2502_09537_b200.device import get_context
+
+pytestmark = pytest.mark.gpu
+SETTINGS = settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+
+
+def _state(g, seed):
+    rng = np.random.default_rng(seed)
+    return kgs.FieldState(*(rng.uniform(-0.5, 0.5, g.M) for _ in range(4)), 0.0)
+
+
+@SETTINGS
+@given(N=st.sampled_from([64, 96, 128]), planes=st.integers(1, 40), steps=st.integers(1, 9),
+       stride=st.integers(1, 4), seed=st.integers(0, 2**31), tau=st.floats(1e-3, 0.05),
+       poison=st.booleans(), plane=st.integers(0, 127))
+def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plane):
+    g = kgs.GridSpec(3, -6.0, 6.0, N)
+    p = kgs.PhysParams(1.1, 0.9, 1.2, 0.8)
+    s0 = _state(g, seed)
+    if poison:
+        s0.V[(plane % N) * N * N + 5] = np.inf
+    outs = []
+    for pipe in (1, 0):
+        ctx = get_context(g, None)
+        ctx.set_param("pipeline", pipe)
+        ctx.set_param("pipeline_planes", planes)
+        s = s0.copy()
+        try:
+            tr = kgs.integrate(s, g, p, kgs.checkerboard_schedule(g), None, tau, steps * tau,
+                               record_stride=stride)
+            outs.append((s, tr.energy, None))
+        except FloatingPointError as e:
+            outs.append((s, None, str(e)))
+    ctx.set_param("pipeline", 1)
+    ctx.set_param("pipeline_planes", 32)
+    (a, ea, xa), (b, eb, xb) = outs
+    assert xa == xb
+    for f in "PQUV":
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+    assert a.t == b.t
+    if ea is not None:
+        np.testing.assert_allclose(ea, eb, rtol=1e-12, atol=1e-300)
+
+
+@SETTINGS
+@given(N=st.sampled_from([64, 128]), slabs=st.sampled_from([2, 4]), steps=st.integers(1, 6),
+       stride=st.integers(0, 3), seed=st.integers(0, 2**31), mirror=st.booleans(),
+       fused=st.booleans(), defer=st.booleans())
+def test_slab_variants_equal_one_slab(N, slabs, steps, stride, seed, mirror, fused, defer):
+    g = kgs.GridSpec(3, -6.0, 6.0, N)
+    p = kgs.PhysParams(0.9, 1.1, 1.0, 0.7)
+    args = kgs.precompute_coefficients(p, 0.01, g).kernel_args()
+    s0 = _state(g, seed)
+    outs = []
+    for ex, params in ((None, {}),
+                       (kgs.CudaExecutor((0,), slabs_per_device=slabs),
+                        {"mirror_halo": int(mirror), "fused_step": int(fused)})):
+        dev = kgs.DeviceFieldState.from_host(s0, g, ex)
+        for k, v in params.items():
+            dev.ctx.set_param(k, v)
+        terms, bad = dev.ctx.step_dpavf2(args, steps, 0, stride, defer_tail=defer)
+        terms2, bad2 = dev.ctx.step_dpavf2(args, 2, steps, stride)
+        outs.append((dev.to_host(), terms, terms2))
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-12, atol=1e-300)
