@@ -507,9 +507,11 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
   if (nrec > 0) std::copy(rec.begin() + NTERMS, rec.end(), terms_out);
   if (bad != ULLONG_MAX) {
     // restore the initial state (device copy) and replay exactly to the bad step
+    // (on the slab stream: a device-to-device cudaMemcpy would not order
+    // itself before the replay's kernels on this non-blocking stream)
     for (int cc = 0; cc < 2; ++cc)
-      CK(cudaMemcpy(s.buf[cc], s.alt[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
-                    cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpyAsync(s.buf[cc], s.alt[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
+                         cudaMemcpyDeviceToDevice, s.stream));
     int64_t fb2 = 0;
     r = KGS_OK;
     if ((int64_t)bad > step_offset)

@@ -310,6 +310,9 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
   CK(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
   CK(cudaEventCreate(&s.ev_t0));
   CK(cudaEventCreate(&s.ev_t1));
+  // the zero-fills above run on the legacy default stream, which the
+  // non-blocking slab streams do not wait for: finish them before any use
+  CK(cudaDeviceSynchronize());
   return KGS_OK;
 }
 

@@ -80,3 +80,59 @@ def test_slab_variants_equal_one_slab(N, slabs, steps, stride, seed, mirror, fus
     assert_bitwise(outs[0][0], outs[1][0])
     np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
     np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-12, atol=1e-300)
+
+
+OPS = st.lists(st.one_of(
+    st.tuples(st.just("steps"), st.integers(1, 4), st.integers(0, 3), st.booleans()),
+    st.tuples(st.just("sweep"), st.sampled_from([0, 1]), st.sampled_from([0, 1])),
+    st.tuples(st.just("energy")),
+    st.tuples(st.just("planes"), st.integers(0, 3), st.integers(0, 63), st.integers(1, 8)),
+    st.tuples(st.just("upload")),
+), min_size=1, max_size=8)
+
+
+@SETTINGS
+@given(N=st.sampled_from([64, 128]), slabs=st.sampled_from([2, 4]), seed=st.integers(0, 2**31),
+       mirror=st.booleans(), fused=st.booleans(), ops=OPS)
+def test_random_operation_sequences_slabs_vs_one(N, slabs, seed, mirror, fused, ops):
+    """Any interleaving of multi-step calls (records, deferred tails), single
+    sweeps, energy evaluations, partial plane uploads and full uploads gives
+    the same bits on several slabs (any knobs) as on one."""
+    g = kgs.GridSpec(3, -6.0, 6.0, N)
+    p = kgs.PhysParams(1.0, 1.2, 0.9, 0.6)
+    args = kgs.precompute_coefficients(p, 0.01, g).kernel_args()
+    s0 = _state(g, seed)
+    rng = np.random.default_rng(seed + 1)
+    fresh = _state(g, seed + 2)
+    outs = []
+    for ex, params in ((None, {}),
+                       (kgs.CudaExecutor((0,), slabs_per_device=slabs),
+                        {"mirror_halo": int(mirror), "fused_step": int(fused)})):
+        dev = kgs.DeviceFieldState.from_host(s0, g, ex)
+        for k, v in params.items():
+            dev.ctx.set_param(k, v)
+        energies, offset = [], 0
+        for op in ops:
+            if op[0] == "steps":
+                _, n, stride, defer = op
+                terms, bad = dev.ctx.step_dpavf2(args, n, offset, stride, defer_tail=defer)
+                assert bad == 0
+                offset += n
+                energies += [float(np.sum(t)) for t in terms]
+            elif op[0] == "sweep":
+                dev.ctx.sweep(op[1], op[2], args)
+            elif op[0] == "energy":
+                energies.append(float(np.sum(dev.energy_terms())))
+            elif op[0] == "planes":
+                _, f, x0, n = op
+                n = min(n, N - x0 % N)
+                x0 = x0 % N
+                plane = g.N * g.N
+                dev.ctx.upload_planes(f, x0, np.ascontiguousarray(
+                    getattr(fresh, "PQUV"[f])[x0 * plane:(x0 + n) * plane]))
+            else:
+                dev.upload(fresh)
+        outs.append((dev.to_host(), energies))
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
