@@ -136,3 +136,47 @@ def test_random_operation_sequences_slabs_vs_one(N, slabs, seed, mirror, fused, 
         dev.close()
     assert_bitwise(outs[0][0], outs[1][0])
     np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
+
+
+@SETTINGS
+@given(d=st.sampled_from([1, 2, 3]), seed=st.integers(0, 2**31), ops=OPS)
+def test_random_operation_sequences_resident_vs_passes(d, seed, ops):
+    """Grids that fit in one CTA's shared memory run whole calls in one
+    launch; any interleaving of calls, sweeps, energy evaluations and
+    uploads gives the same bits as the per-pass kernels."""
+    N = {1: 256, 2: 32, 3: 12}[d]
+    g = kgs.GridSpec(d, -6.0, 6.0, N)
+    p = kgs.PhysParams(1.0, 1.2, 0.9, 0.6)
+    args = kgs.precompute_coefficients(p, 0.01, g).kernel_args()
+    s0 = _state(g, seed)
+    fresh = _state(g, seed + 2)
+    plane = g.M // (N if d > 1 else 1)
+    nplanes = N if d > 1 else 1
+    outs = []
+    for resident in (1, 0):
+        dev = kgs.DeviceFieldState.from_host(s0, g)
+        dev.ctx.set_param("resident", resident)
+        energies, offset = [], 0
+        for op in ops:
+            if op[0] == "steps":
+                _, n, stride, defer = op
+                terms, bad = dev.ctx.step_dpavf2(args, n, offset, stride, defer_tail=defer)
+                assert bad == 0
+                offset += n
+                energies += [float(np.sum(t)) for t in terms]
+            elif op[0] == "sweep":
+                dev.ctx.sweep(op[1], op[2], args)
+            elif op[0] == "energy":
+                energies.append(float(np.sum(dev.energy_terms())))
+            elif op[0] == "planes":
+                _, f, x0, n = op
+                x0 = x0 % nplanes
+                n = min(n, nplanes - x0)
+                dev.ctx.upload_planes(f, x0, np.ascontiguousarray(
+                    getattr(fresh, "PQUV"[f])[x0 * plane:(x0 + n) * plane]))
+            else:
+                dev.upload(fresh)
+        outs.append((dev.to_host(), energies))
+        dev.close()
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
