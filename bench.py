@@ -184,7 +184,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * cb["seconds"] / steps,
-        "higher_is_better": True, "scaling": "strong" if args.scaling == "strong" else "weak",
+        "higher_is_better": True,
+        "scaling": "weak" if (args.scaling == "weak" and round(world ** (1 / 3)) ** 3 == world)
+                   else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"3D KGS {SCENARIO} N={N}^3 fp64, tau={TAU}, checkerboard DP-AVF2",
                    "sample": cb["sample"]},
