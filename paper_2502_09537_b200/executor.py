@@ -48,7 +48,20 @@ class ExecutorConfig:
             return SerialExecutor()
         if self.mode == "phased":
             return PhasedExecutor(self.workers)
-        return CudaExecutor(tuple(range(self.workers)))
+        # one slab per GPU; with fewer GPUs than workers, virtual slabs on
+        # cuda:0 (same results bitwise: decomposition invariance)
+        n = _device_count()
+        if self.workers <= max(n, 1) or n == 0:
+            return CudaExecutor(tuple(range(self.workers)))
+        return CudaExecutor((0,), slabs_per_device=self.workers)
+
+
+def _device_count() -> int:
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
 
 
 class _DeviceExecutor:

@@ -251,3 +251,13 @@ class TestExecutorRun:
         g = self._grid()
         with pytest.raises(TypeError):
             kgs.CudaExecutor((0,)).run(kgs.checkerboard_schedule(g), lambda lane: None)
+
+
+def test_cuda_executor_config_uses_virtual_slabs_beyond_the_gpu_count(monkeypatch):
+    from paper_2502_09537_b200 import executor as exm
+    monkeypatch.setattr(exm, "_device_count", lambda: 1)
+    ex = kgs.ExecutorConfig("cuda", 4).build()
+    assert ex.devices == (0,) and ex.slabs_per_device == 4 and ex.nslabs == 4
+    monkeypatch.setattr(exm, "_device_count", lambda: 8)
+    ex = kgs.ExecutorConfig("cuda", 4).build()
+    assert ex.devices == (0, 1, 2, 3) and ex.slabs_per_device == 1
