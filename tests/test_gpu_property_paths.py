@@ -60,12 +60,15 @@ def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plan
 @SETTINGS
 @given(N=st.sampled_from([64, 128]), slabs=st.sampled_from([2, 4]), steps=st.integers(1, 6),
        stride=st.integers(0, 3), seed=st.integers(0, 2**31), mirror=st.booleans(),
-       fused=st.booleans(), defer=st.booleans())
-def test_slab_variants_equal_one_slab(N, slabs, steps, stride, seed, mirror, fused, defer):
+       fused=st.booleans(), defer=st.booleans(), poison=st.one_of(st.none(), st.integers(0, 127)))
+def test_slab_variants_equal_one_slab(N, slabs, steps, stride, seed, mirror, fused, defer,
+                                      poison):
     g = kgs.GridSpec(3, -6.0, 6.0, N)
     p = kgs.PhysParams(0.9, 1.1, 1.0, 0.7)
     args = kgs.precompute_coefficients(p, 0.01, g).kernel_args()
     s0 = _state(g, seed)
+    if poison is not None:   # a non-finite value on any plane, incl. slab faces
+        s0.U[(poison % N) * N * N + 3] = np.nan
     outs = []
     for ex, params in ((None, {}),
                        (kgs.CudaExecutor((0,), slabs_per_device=slabs),
@@ -75,11 +78,16 @@ def test_slab_variants_equal_one_slab(N, slabs, steps, stride, seed, mirror, fus
             dev.ctx.set_param(k, v)
         terms, bad = dev.ctx.step_dpavf2(args, steps, 0, stride, defer_tail=defer)
         terms2, bad2 = dev.ctx.step_dpavf2(args, 2, steps, stride)
-        outs.append((dev.to_host(), terms, terms2))
+        outs.append((dev.to_host(), terms, terms2, bad, bad2))
         dev.close()
-    assert_bitwise(outs[0][0], outs[1][0])
-    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
-    np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-12, atol=1e-300)
+    assert_bitwise(outs[0][0], outs[1][0], equal_nan=True)
+    assert outs[0][3:] == outs[1][3:]
+    if poison is None:
+        assert outs[0][3] == 0
+        np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-12, atol=1e-300)
+    else:
+        assert outs[0][3] == 1
 
 
 OPS = st.lists(st.one_of(
