@@ -223,8 +223,12 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
  * -- runs a whole kgs_step_dpavf2 call in one launch; 0: per-pass
  * launches), "mirror_halo" (1, the default: single-process slabs store
  * their faces from the boundary launches straight into the neighbours'
- * ghost planes; 0: peer copies after each pass).  KGS_EINVAL for unknown
- * names. */
+ * ghost planes; 0: peer copies after each pass), "tma_store" (marching
+ * kernel's own-tile write: 0 per-thread stores, 1 one TMA bulk store, 2,
+ * the default, bulk store with an L2 evict-first hint), "pipeline" (1, the
+ * default: kgs_integrate_host overlaps upload, passes and download on one
+ * slab; 0: in sequence), "pipeline_planes" (its chunk, default 32 planes).
+ * KGS_EINVAL for unknown names. */
 int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 
 /* L2 sector promotion of the marching kernel's TMA boxes (0 none, 1 64 B,
