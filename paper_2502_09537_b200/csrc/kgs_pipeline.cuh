@@ -32,7 +32,10 @@ int ensure_alt(kgs_ctx* ctx) {
       if (s.alt[c]) continue;
       if (cudaMalloc(&s.alt[c], colour_bytes) != cudaSuccess) {
         cudaGetLastError();
-        s.alt[c] = nullptr;
+        for (int cc = 0; cc < 2; ++cc) {   // do not hold half a buffer set
+          if (s.alt[cc]) cudaFree(s.alt[cc]);
+          s.alt[cc] = s.alt0[cc] = nullptr;
+        }
         return KGS_ENOMEM;
       }
       s.alt0[c] = s.alt[c] + ctx->ps;
