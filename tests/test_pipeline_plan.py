@@ -78,3 +78,13 @@ def test_pipeline_plan_headline_shape():
 def test_pipeline_plan_rejects_bad_arguments():
     assert _lib.load().kgs_pipeline_plan(0, 32, 1, None, 0) == -1
     assert _lib.load().kgs_pipeline_plan(64, 0, 1, None, 0) == -1
+
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=300, deadline=None)
+@given(N=st.integers(2, 300), C=st.integers(1, 80), nsteps=st.integers(0, 30))
+def test_pipeline_plan_random_shapes(N, C, nsteps):
+    check(N, C, nsteps)
