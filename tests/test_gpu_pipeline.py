@@ -88,3 +88,33 @@ def test_pipeline_device_state_after_call_is_the_result():
     z = kgs.FieldState.zeros(g)
     get_context(g, None).download(z)
     assert_bitwise(z, ref)
+
+
+@pytest.mark.parametrize("offset,steps,stride", [(3, 5, 2), (7, 4, 3), (1, 6, 6), (10, 2, 4)])
+def test_integrate_host_step_offset_matches_step_dpavf2(offset, steps, stride):
+    """The C ABI's step_offset: records land on global steps multiple of the
+    stride, exactly as kgs_step_dpavf2 numbers them."""
+    import ctypes
+    from paper_2502_09537_b200 import _lib
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    nrec = (offset + steps) // stride - offset // stride
+    ctx = get_context(g, None)
+    a = s0.copy()
+    c = _lib.coeffs_struct(args)
+    t0 = np.zeros(8)
+    terms = np.zeros((max(nrec, 1), 8))
+    bad = ctypes.c_int64()
+    rc = _lib.load().kgs_integrate_host(ctx.ptr, *(_lib.dptr(getattr(a, f)) for f in "PQUV"),
+                                        ctypes.byref(c), steps, offset, stride,
+                                        _lib.dptr(t0), _lib.dptr(terms), ctypes.byref(bad), 0)
+    assert rc == 0
+    dev = kgs.DeviceFieldState.from_host(s0, g)
+    ref_terms, b2 = dev.ctx.step_dpavf2(args, steps, offset, stride)
+    b = dev.to_host()
+    dev.close()
+    assert b2 == 0
+    assert_bitwise(a, b)
+    np.testing.assert_allclose(terms[:nrec], ref_terms, rtol=1e-13, atol=0)
