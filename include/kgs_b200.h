@@ -238,8 +238,8 @@ int kgs_set_promotion(kgs_ctx* ctx, int halo, int tile);
 
 /* Benchmarking only (CORRUPTS the resident state): average device time of
  * `reps` black fused passes of the marching kernel in a debug mode:
- * 0 = normal, 1 = no arithmetic (data movement only), 2 = no ghost-cell
- * stores, 3 = no stores.  Used to measure the pass's memory ceiling. */
+ * 0 = normal, 1 = no arithmetic (data movement only), 2 or 3 = no stores.
+ * Used to measure the pass's memory ceiling. */
 int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out);
 
 /* Device self-test: the shared-reciprocal division used by the kernels

@@ -1,5 +1,5 @@
 """Memory ceiling of the marching pass: time the black fused pass in debug
-modes (0 normal, 1 no arithmetic, 2 no ghost stores, 3 no stores).
+modes (0 normal, 1 no arithmetic, 3 no stores).
 Corrupts the state (benchmark only).   python tools/debug_ceiling.py [--N 1024]"""
 import argparse
 import ctypes

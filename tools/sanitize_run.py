@@ -1,5 +1,7 @@
-"""Small runs of every kernel family for compute-sanitizer (memcheck /
-racecheck / synccheck):
+"""Small runs of every kernel family, for compute-sanitizer (memcheck /
+racecheck / synccheck) where it is available, or with the index-asserting
+build (python -m paper_2502_09537_b200.build --checked;
+KGS_B200_LIB=paper_2502_09537_b200/libkgs_b200_checked.so):
   resident kernel (8^3), march passes (64^3, 1 slab), virtual slabs with
   fused halo stores (64^3, 4 slabs) and copies, the opt-in fused step
   (64^3, 1 and 2 slabs), 2-D and 1-D per-pass kernels, energy/finiteness
