@@ -118,3 +118,22 @@ def test_integrate_host_step_offset_matches_step_dpavf2(offset, steps, stride):
     assert b2 == 0
     assert_bitwise(a, b)
     np.testing.assert_allclose(terms[:nrec], ref_terms, rtol=1e-13, atol=0)
+
+
+def test_integrate_nonfinite_on_slabs_matches_one_slab():
+    """integrate() on a host state with several slabs takes kgs_integrate_host's
+    plain path; a non-finite step leaves the same state and message as one slab."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(64)
+    s0 = sc.state(g)
+    s0.P[40 * 64 * 64 + 9] = np.nan
+    outs = []
+    for ex in (None, kgs.CudaExecutor((0,), slabs_per_device=2),
+               kgs.CudaExecutor((0,), slabs_per_device=4)):
+        s = s0.copy()
+        with pytest.raises(FloatingPointError) as err:
+            kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), ex, 0.01, 0.05)
+        outs.append((s, str(err.value)))
+    for s, msg in outs[1:]:
+        assert msg == outs[0][1]
+        assert_bitwise(s, outs[0][0], equal_nan=True)
