@@ -137,3 +137,44 @@ def test_integrate_nonfinite_on_slabs_matches_one_slab():
     for s, msg in outs[1:]:
         assert msg == outs[0][1]
         assert_bitwise(s, outs[0][0], equal_nan=True)
+
+
+def _pinned_copy(g, s):
+    p = kgs.FieldState.pinned(g)
+    for f in "PQUV":
+        getattr(p, f)[:] = getattr(s, f)
+    p.t = s.t
+    return p
+
+
+@pytest.mark.parametrize("N,steps,stride,planes,poison", [
+    (256, 6, 3, 32, None), (256, 5, 1, 7, None), (512, 8, 4, 32, None),
+    (256, 4, 2, 16, 130), (256, 3, 3, 32, 0)])
+def test_pipeline_with_pinned_host_arrays(N, steps, stride, planes, poison):
+    """Page-locked host arrays make the pipeline's copies truly asynchronous
+    (the bench's e2e case): still bitwise the plain path, incl. the replay."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(N)
+    s0 = sc.state(g)
+    if poison is not None:
+        s0.U[poison * N * N + 11] = np.inf
+    outs = []
+    for pipe in (1, 0):
+        ctx = get_context(g, None)
+        ctx.set_param("pipeline", pipe)
+        ctx.set_param("pipeline_planes", planes)
+        s = _pinned_copy(g, s0)
+        try:
+            tr = kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, 0.01,
+                               steps * 0.01, record_stride=stride)
+            res = (tr.energy, None)
+        except FloatingPointError as e:
+            res = (None, str(e))
+        outs.append((s.copy(), res))
+    ctx.set_param("pipeline", 1)
+    ctx.set_param("pipeline_planes", 32)
+    (a, (ea, xa)), (b, (eb, xb)) = outs
+    assert xa == xb
+    assert_bitwise(a, b, equal_nan=True)
+    if ea is not None:
+        np.testing.assert_allclose(ea, eb, rtol=1e-13, atol=0)
