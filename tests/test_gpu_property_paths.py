@@ -27,8 +27,8 @@ def _state(g, seed):
 @SETTINGS
 @given(N=st.sampled_from([64, 96, 128]), planes=st.integers(1, 40), steps=st.integers(1, 9),
        stride=st.integers(1, 4), seed=st.integers(0, 2**31), tau=st.floats(1e-3, 0.05),
-       poison=st.booleans(), plane=st.integers(0, 127))
-def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plane):
+       poison=st.booleans(), plane=st.integers(0, 127), pinned=st.booleans())
+def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plane, pinned):
     g = kgs.GridSpec(3, -6.0, 6.0, N)
     p = kgs.PhysParams(1.1, 0.9, 1.2, 0.8)
     s0 = _state(g, seed)
@@ -40,12 +40,16 @@ def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plan
         ctx.set_param("pipeline", pipe)
         ctx.set_param("pipeline_planes", planes)
         s = s0.copy()
+        if pinned:   # page-locked arrays: truly asynchronous copies in the pipeline
+            s = kgs.FieldState.pinned(g)
+            for f in "PQUV":
+                getattr(s, f)[:] = getattr(s0, f)
         try:
             tr = kgs.integrate(s, g, p, kgs.checkerboard_schedule(g), None, tau, steps * tau,
                                record_stride=stride)
-            outs.append((s, tr.energy, None))
+            outs.append((s.copy(), tr.energy, None))
         except FloatingPointError as e:
-            outs.append((s, None, str(e)))
+            outs.append((s.copy(), None, str(e)))
     ctx.set_param("pipeline", 1)
     ctx.set_param("pipeline_planes", 32)
     (a, ea, xa), (b, eb, xb) = outs
