@@ -287,7 +287,8 @@ int kgs_download(kgs_ctx* ctx, double* P, double* Q, double* U, double* V) {
 int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
                       const double* src) {
   int r = check_range(ctx, field, x_begin, nplanes, src);
-  if (!r) r = flush_pending(ctx);
+  if (r) return r;
+  r = flush_pending(ctx);
   if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, const_cast<double*>(src), true);
   ctx->mirrored[0] = ctx->mirrored[1] = false;  // planes written without mirroring
   if (!r && field < 3) r = exchange(ctx, 0);   // refresh faces (P, Q, U are halo fields)
@@ -445,7 +446,7 @@ int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
 }
 
 int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap) {
-  if (N < 1 || C < 1 || nsteps < 0) return -1;
+  if (N < 1 || C < 1 || nsteps < 0 || cap < 0 || (cap > 0 && !out)) return -1;
   const std::vector<PipeEvent> plan = pipeline_plan(N, C, pipeline_shrinks(nsteps));
   const int64_t n = (int64_t)plan.size();
   for (int64_t i = 0; i < std::min(n, cap); ++i) {
@@ -595,7 +596,10 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   CK(cudaSetDevice(s.dev));
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
-  CK(cudaEventCreate(&b));
+  if (cudaEventCreate(&b) != cudaSuccess) {
+    cudaEventDestroy(a);
+    return fail(ctx, KGS_ECUDA, "cudaEventCreate failed");
+  }
   int r = KGS_OK;
   for (int i = 0; i <= reps && !r; ++i) {
     if (i == 1) CK(cudaEventRecord(a, s.stream));
@@ -609,14 +613,17 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
     }
 #undef KGS_DBG
   }
-  CK(cudaEventRecord(b, s.stream));
-  CK(cudaEventSynchronize(b));
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaError_t e = cudaSuccess;
+  if (!r) e = cudaEventRecord(b, s.stream);
+  if (!r && e == cudaSuccess) e = cudaEventSynchronize(b);
+  if (!r && e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
   cudaEventDestroy(a);
   cudaEventDestroy(b);
+  if (r) return r;
+  if (e != cudaSuccess) return fail(ctx, KGS_ECUDA, "debug pass: %s", cudaGetErrorString(e));
   *ms_out = ms / reps;
-  return r;
+  return KGS_OK;
 }
 
 int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatches) {

@@ -63,6 +63,41 @@ def test_create_rejects_bad_geometry_before_touching_a_device():
     assert not ptr.value
 
 
+def test_null_arguments_are_rejected_without_touching_a_device():
+    """Every entry point taking a context returns KGS_EINVAL for NULL
+    arguments (no crash, no CUDA call), like the reference's ValueErrors."""
+    lib = _lib.load()
+    E = _lib.KGS_EINVAL
+    buf = (ctypes.c_double * 8)()
+    i64 = ctypes.c_int64()
+    assert lib.kgs_upload(None, buf, buf, buf, buf) == E
+    assert lib.kgs_download(None, buf, buf, buf, buf) == E
+    assert lib.kgs_upload_planes(None, 0, 0, 1, buf) == E
+    assert lib.kgs_download_planes(None, 0, 0, 1, buf) == E
+    assert lib.kgs_sweep(None, 0, 0, None) == E
+    assert lib.kgs_step_dpavf2(None, None, 1, 0, 0, None, ctypes.byref(i64), 0) == E
+    assert lib.kgs_integrate_host(None, buf, buf, buf, buf, None, 1, 0, 0, buf, buf,
+                                  ctypes.byref(i64), 0) == E
+    assert lib.kgs_energy_terms(None, buf) == E
+    assert lib.kgs_energy_mass(None, 1.0, 1.0, 1.0, 1.0, buf, buf) == E
+    assert lib.kgs_all_finite(None, ctypes.byref(ctypes.c_int())) == E
+    assert lib.kgs_fill_preset(None, 0) == E
+    assert lib.kgs_local_range(None, None, None, None) == E
+    assert lib.kgs_set_param(None, b"pipeline", 1) == E
+    assert lib.kgs_set_tuning(None, 4, 0, 0, 0, -1) == E
+    assert lib.kgs_set_promotion(None, 0, 0) == E
+    assert lib.kgs_pass_timing(None, 1) == E
+    assert lib.kgs_pass_stats(None, None, None, None) == E
+    assert lib.kgs_upload_planes(None, 0, 0, 1, buf) == E
+    assert b"NULL" in lib.kgs_last_error(None)
+    assert lib.kgs_debug_pass(None, 0, 1, buf) == E
+    assert lib.kgs_destroy(None) == _lib.KGS_OK
+    assert lib.kgs_launch_count(None) == 0
+    # the plan query validates its output buffer too
+    assert lib.kgs_pipeline_plan(64, 8, 2, None, 10) == -1
+    assert lib.kgs_pipeline_plan(64, 8, 2, None, 0) > 0
+
+
 @pytest.mark.skipif(_have_gpu(), reason="checks the no-GPU failure path")
 def test_device_entry_points_fail_loudly_without_gpu():
     g = kgs.GridSpec(2, -1.0, 1.0, 8)
