@@ -39,6 +39,7 @@ METRIC = "3D KGS grid-point updates/s at 1/2/4/8 B200; % of HBM roofline vs CPU 
 UNIT = "point-updates/s"
 BYTES_PER_UPDATE = 64          # P,Q,U,V read+write once per update
 DESIGN_BYTES_PER_UPDATE = 44   # colour-split fused passes
+DIAG_STEPS = 5                # steps of the record-every-step run (diagnostics price)
 TAU = 0.01
 SCENARIO = "ellipsoids3d"
 
@@ -266,6 +267,23 @@ def run_ours(args):
     # energy sanity (the timed run recorded step W+K)
     e = kgs.grid.energy_from_terms(terms[0], sc.params, g)[0] if len(terms) else None
 
+    # price of the diagnostics (SURVEY.md §7 timed runs): a few more steps with
+    # an energy/mass record after EVERY step, the reference's record_stride=1
+    R = DIAG_STEPS
+    barrier(world)
+    terms_r, bad_r = ctx.step_dpavf2(kargs, R, W + K, 1)
+    ms_r = max_over_ranks(ctx.last_step_ms(), world)
+    if bad_r:
+        raise FloatingPointError(f"non-finite state at step {bad_r}")
+    em = [kgs.grid.energy_from_terms(t, sc.params, g) for t in [terms[-1], *terms_r]]
+    diag = {"record_stride": 1, "steps": R, "ms_per_step": ms_r / R,
+            "value": 2.0 * g.M * R / (ms_r / 1e3), "unit": UNIT,
+            "cost_vs_unrecorded": (ms_r / R) / (ms / K),
+            "max_rel_energy_change": max(abs(E - em[0][0]) / abs(em[0][0]) for E, _ in em),
+            "max_rel_mass_change": max(abs(m - em[0][1]) / abs(em[0][1]) for _, m in em),
+            "note": "energy is the scheme's invariant (round-off drift); mass is not conserved "
+                    "by DP-AVF2 and drifts at the reference's own rate (grows with N)"}
+
     # e2e through the public API: integrate() on a pinned host state
     e2e = None
     if not args.no_e2e:
@@ -315,6 +333,7 @@ def run_ours(args):
                    "parallelism": f"slab{world}", "l2": "inputs (32 GiB state) >> L2 (126 MB)",
                    "record_stride": K},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
+        "diagnostics": diag,
         "clocks": clk.summary(), "wall_s": wall, "energy_final": e,
         "pct_hbm_roofline": 100.0 * roof["frac"],
     }
