@@ -259,9 +259,11 @@ def get_context(grid: GridSpec, executor=None) -> DeviceContext:
     plan = resolve(executor)
     key = (grid.d, grid.a, grid.b, grid.N) + plan.key()
     ctx = _CTX_CACHE.get(key)
-    if ctx is not None:
+    if ctx is not None and ctx.ptr.value:
         _CTX_CACHE.move_to_end(key)
         return ctx
+    if ctx is not None:   # closed by its user (DeviceFieldState.close): replace it
+        del _CTX_CACHE[key]
     while len(_CTX_CACHE) >= _CTX_CACHE_MAX:
         _, old = _CTX_CACHE.popitem(last=False)
         old.close()

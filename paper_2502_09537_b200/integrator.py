@@ -138,9 +138,15 @@ class EnergyTrace:
         return max(self.rel_error)
 
 
-def _pipeline_ok(host) -> bool:
-    return all(getattr(host, f).dtype == np.float64 and getattr(host, f).flags["C_CONTIGUOUS"]
-               for f in "PQUV")
+def _pipeline_ok(host, grid: GridSpec) -> bool:
+    """The one-call path hands the host arrays to C as raw pointers: they must
+    be whole-grid, contiguous, writable float64 (else the checked path runs)."""
+    for f in "PQUV":
+        a = getattr(host, f)
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.shape == (grid.M,)
+                and a.flags["C_CONTIGUOUS"] and a.flags["WRITEABLE"]):
+            return False
+    return True
 
 
 def _append_records(trace, terms, k0, k1, record_stride, t, e0, absolute, params, grid,
@@ -193,7 +199,7 @@ def integrate(state, grid: GridSpec, params: PhysParams,
             t += coeffs_half.tau
         return t
 
-    if host is not None and not snap and n_steps > 0 and _pipeline_ok(host):
+    if host is not None and not snap and n_steps > 0 and _pipeline_ok(host, grid):
         ctx = get_context(grid, executor)
         if not ctx.dist:
             # one call: upload | steps | download overlapped (kgs_integrate_host)

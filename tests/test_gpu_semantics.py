@@ -136,3 +136,16 @@ class TestIntegrateBookkeeping:
         g, p, s, sch = self._setup()
         tr = kgs.integrate(s, g, p, sch, None, 0.05, 2.0)
         assert tr.max_rel_error() <= 1e-12 and tr.rel_error[0] == 0.0
+
+
+def test_closed_cached_context_is_replaced():
+    """A temporary device state shares the cached context of its grid;
+    closing it must not poison later host-state calls on that grid."""
+    from paper_2502_09537_b200.device import as_device_state
+    g = kgs.GridSpec(2, 0.0, 4.0, 16)
+    s = kgs.seeded_random_state(g, 3, 0.5)
+    e0 = kgs.discrete_energy(s, kgs.PhysParams(), g)
+    dev, temporary = as_device_state(s, g)
+    assert temporary
+    dev.close()                       # closes the cached context
+    assert kgs.discrete_energy(s, kgs.PhysParams(), g) == e0

@@ -296,3 +296,22 @@ def test_cuda_executor_config_uses_virtual_slabs_beyond_the_gpu_count(monkeypatc
     monkeypatch.setattr(exm, "_device_count", lambda: 8)
     ex = kgs.ExecutorConfig("cuda", 4).build()
     assert ex.devices == (0, 1, 2, 3) and ex.slabs_per_device == 1
+
+
+def test_one_call_path_only_takes_whole_grid_writable_float64():
+    """integrate() hands host arrays to kgs_integrate_host as raw pointers;
+    anything else must take the shape-checked path."""
+    from paper_2502_09537_b200.integrator import _pipeline_ok
+    g = kgs.GridSpec(2, 0.0, 1.0, 8)
+    s = kgs.FieldState.zeros(g)
+    assert _pipeline_ok(s, g)
+    assert not _pipeline_ok(s, kgs.GridSpec(2, 0.0, 1.0, 16))      # too small for the grid
+    bad = kgs.FieldState.zeros(g)
+    bad.U = np.zeros(2 * g.M)[::2]                                   # strided view
+    assert not _pipeline_ok(bad, g)
+    ro = kgs.FieldState.zeros(g)
+    ro.V.flags.writeable = False
+    assert not _pipeline_ok(ro, g)
+    f32 = kgs.FieldState.zeros(g)
+    f32.P = np.zeros(g.M, dtype=np.float32)
+    assert not _pipeline_ok(f32, g)
