@@ -214,6 +214,11 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   if (ctx->tune_band_rows <= 0) nbt = g.nyt;  // no banding
   g.nbt = nbt;
   g.ntiles = (int64_t)(xb - xa) * g.nyt * g.nkt;
+  g.fd_band = make_fastdiv((unsigned)std::max<int64_t>(1, (int64_t)(xb - xa) * nbt * g.nkt));
+  g.fd_plane = make_fastdiv((unsigned)(nbt * g.nkt));
+  g.fd_nkt = make_fastdiv((unsigned)g.nkt);
+  g.fd_nk = make_fastdiv((unsigned)ctx->nk);
+  g.fd_ny = make_fastdiv((unsigned)ctx->ny);
   return g;
 }
 

@@ -152,7 +152,9 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     return kPipeFallback;
   Slab& s = ctx->slabs[0];
   const int64_t N = s.nx;
-  const int64_t C = std::max<int64_t>(1, ctx->tune_pipe_chunk);
+  // chunk planes; a layout-transform launch covers < 2^31 point pairs (decode_point)
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(ctx->tune_pipe_chunk,
+                                                           ((1ll << 31) - 1) / ((int64_t)ctx->ny * ctx->nk)));
   const int64_t nb = (N + C - 1) / C;
   if (nb < 4) return kPipeFallback;
   const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;

@@ -9,9 +9,12 @@ C3: 3-D ellipsoids3d N=512^3, tau=0.01
 Prints one JSON line with ms/step and updates/s per config.
 """
 import json
+import sys
 import time
+from pathlib import Path
 
-import paper_2502_09537_b200 as kgs
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2502_09537_b200 as kgs  # noqa: E402
 
 
 def rate(name, N, tau, steps, stride):
