@@ -122,6 +122,7 @@ struct kgs_ctx {
   int tune_fused_dbg = 0;  // fused step timing experiments (results invalid)
   int tune_resident = 1;   // small grids: whole call in one launch (shared memory)
   int tune_tstore = 2;
+  int tune_pdl = 1;          // colour passes: programmatic dependent launch
   int tune_pipe = 1;         // kgs_integrate_host: overlap upload | passes | download
   int tune_pipe_chunk = 32;  // planes per transfer chunk     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
   // fused halo exchange (single-process slabs): boundary launches

@@ -672,6 +672,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "pipeline") ctx->tune_pipe = value;
   else if (n == "pipeline_planes") ctx->tune_pipe_chunk = std::max(1, value);
   else if (n == "mirror_halo") ctx->tune_mirror = value;
+  else if (n == "pdl") ctx->tune_pdl = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);
   return KGS_OK;
 }

@@ -18,8 +18,22 @@ int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
   int64_t grid = std::min<int64_t>(g.ntiles, (int64_t)bps * ctx->nsm);
   grid = std::min<int64_t>(grid, ctx->grid_cap);
   if (grid < 1) return KGS_OK;  // nothing to do
-  kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(
-      g, c, s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no);
+  double* part = s.partials[COL] + (int64_t)s.npart[COL] * NTERMS;
+  if (ctx->tune_pdl) {   // overlap this launch with the previous pass's drain
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, g, c, part, s.bad, step_no));
+  } else {
+    kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(g, c, part, s.bad, step_no);
+  }
   ctx->launches++;
   if (DIAG) s.npart[COL] += (int)grid;
   CK(cudaGetLastError());
