@@ -228,9 +228,9 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
  * the default, bulk store with an L2 evict-first hint), "pipeline" (1, the
  * default: kgs_integrate_host overlaps upload, passes and download on one
  * slab; 0: in sequence), "pipeline_planes" (its chunk, default 32 planes),
- * "pdl" (1, the default: the per-point colour passes of 1-D/2-D/small grids
- * are launched as programmatic dependents of the previous pass, so their
- * launch overlaps its drain; 0: plain stream order).
+ * "pdl" (1, the default: the colour passes and record reductions are
+ * launched as programmatic dependents of the previous kernel on the stream,
+ * so their launch and set-up overlap its drain; 0: plain stream order).
  * KGS_EINVAL for unknown names. */
 int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 

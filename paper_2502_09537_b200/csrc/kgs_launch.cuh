@@ -5,6 +5,29 @@
 namespace {
 
 // ---- kernel dispatch -----------------------------------------------------
+// Launch a kernel that opens with griddepcontrol.wait / launch_dependents as
+// a programmatic dependent of the previous kernel on the stream (its launch
+// and CTA dispatch overlap that kernel's drain), or in plain stream order.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_dependent(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block,
+                             size_t smem, cudaStream_t stream, Args... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, stream>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int D, int COL, int OP1, int OP2, bool DIAG, bool CHECK>
 int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
              int step_no) {
@@ -19,21 +42,8 @@ int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
   grid = std::min<int64_t>(grid, ctx->grid_cap);
   if (grid < 1) return KGS_OK;  // nothing to do
   double* part = s.partials[COL] + (int64_t)s.npart[COL] * NTERMS;
-  if (ctx->tune_pdl) {   // overlap this launch with the previous pass's drain
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s.stream;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, g, c, part, s.bad, step_no));
-  } else {
-    kern<<<(unsigned)grid, kThreads, 0, s.stream>>>(g, c, part, s.bad, step_no);
-  }
+  CK(launch_dependent(ctx->tune_pdl != 0, kern, (unsigned)grid, kThreads, 0, s.stream, g, c,
+                      part, s.bad, step_no));
   ctx->launches++;
   if (DIAG) s.npart[COL] += (int)grid;
   CK(cudaGetLastError());
@@ -227,9 +237,9 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
                           s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no,
                           mc));
   } else {
-    kern<<<(unsigned)grid, Var::NT, L::bytes, s.stream>>>(
-        s.maps[v][COL ^ 1], s.maps[v][COL], g, c,
-        s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no, mc);
+    CK(launch_dependent(ctx->tune_pdl != 0, kern, (unsigned)grid, (unsigned)Var::NT, L::bytes,
+                        s.stream, s.maps[v][COL ^ 1], s.maps[v][COL], g, c,
+                        s.partials[COL] + (int64_t)s.npart[COL] * NTERMS, s.bad, step_no, mc));
   }
   ctx->launches++;
   if (DIAG) s.npart[COL] += (int)grid;

@@ -217,11 +217,11 @@ int collect_pass_times(kgs_ctx* ctx) {
 int finalize_record(kgs_ctx* ctx, int64_t slot, bool both) {
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
-    finalize_terms<<<1, kThreads, 0, s.stream>>>(
-        s.partials[1], s.npart[1], both ? s.partials[0] : nullptr,
-        both ? s.npart[0] : 0, s.records + slot * NTERMS);
+    CK(launch_dependent(ctx->tune_pdl != 0, finalize_terms, 1u, (unsigned)kThreads, 0, s.stream,
+                        (const double*)s.partials[1], s.npart[1],
+                        (const double*)(both ? s.partials[0] : nullptr), both ? s.npart[0] : 0,
+                        s.records + slot * NTERMS));
     ctx->launches++;
-    CK(cudaGetLastError());
   }
   return KGS_OK;
 }

@@ -151,11 +151,13 @@ def test_closed_cached_context_is_replaced():
     assert kgs.discrete_energy(s, kgs.PhysParams(), g) == e0
 
 
-@pytest.mark.parametrize("d,N", [(1, 4096), (2, 96), (3, 32)])
-def test_programmatic_dependent_launch_is_bitwise_neutral(d, N):
-    """The per-point colour passes launched as programmatic dependents of the
-    previous pass (knob "pdl", default on) give the plain stream-ordered
-    result bit for bit, records included."""
+@pytest.mark.parametrize("d,N,march", [(1, 4096, False), (2, 96, False), (3, 32, False),
+                                       (3, 64, True)])
+def test_programmatic_dependent_launch_is_bitwise_neutral(d, N, march):
+    """The colour passes (per-point and marching) and the record reductions
+    launched as programmatic dependents of the previous kernel (knob "pdl",
+    default on) give the plain stream-ordered result bit for bit, records
+    included."""
     g = kgs.GridSpec(d, -4.0, 4.0, N)
     s = kgs.seeded_random_state(g, 5, 0.5)
     a = kgs.precompute_coefficients(kgs.PhysParams(), 0.01, g).kernel_args()
@@ -163,7 +165,8 @@ def test_programmatic_dependent_launch_is_bitwise_neutral(d, N):
     for pdl in (0, 1):
         dev = _dev(s, g)
         dev.ctx.set_param("resident", 0)
-        dev.ctx.set_param("march_planes", -1)     # per-point kernel for every d
+        if not march:
+            dev.ctx.set_param("march_planes", -1)     # per-point kernel for every d
         dev.ctx.set_param("pdl", pdl)
         terms, bad = dev.ctx.step_dpavf2(a, 7, 0, 2)
         res.append((dev.to_host(), terms, bad))
