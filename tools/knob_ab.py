@@ -2,12 +2,17 @@
 (1 GPU, resident state): average live pass time per setting, and the fields
 must come out bitwise identical for every setting.
 
-    python tools/knob_ab.py KNOB V0,V1[,..] [--N 1024] [--steps 6] [--reps 4]
+    python tools/knob_ab.py KNOB V0,V1[,..] [--N 1024] [--steps 6] [--reps 4] [--call]
+
+--call times the whole kgs_step_dpavf2 call (host wall clock around the
+synchronous call, one untimed warm-up call first) instead of the per-pass
+events, so launch overlap between passes (e.g. the `pdl` knob) is included.
 """
 import argparse
 import hashlib
 import json
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -21,6 +26,7 @@ def main():
     ap.add_argument("--N", type=int, default=1024)
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--call", action="store_true")
     a = ap.parse_args()
     vals = [int(v) for v in a.values.split(",")]
     sc = kgs.get_scenario("ellipsoids3d")
@@ -32,10 +38,16 @@ def main():
         for v in vals:
             dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
             dev.ctx.set_param(a.knob, v)
-            dev.ctx.pass_timing(True)
-            dev.ctx.step_dpavf2(args, a.steps, 0, a.steps)
-            n, ms, _ = dev.ctx.pass_stats()
-            times[v].append(ms / n)
+            if a.call:
+                dev.ctx.step_dpavf2(args, 2, 0, 2)
+                t0 = time.perf_counter()
+                dev.ctx.step_dpavf2(args, a.steps, 0, a.steps)
+                times[v].append((time.perf_counter() - t0) * 1e3 / a.steps)
+            else:
+                dev.ctx.pass_timing(True)
+                dev.ctx.step_dpavf2(args, a.steps, 0, a.steps)
+                n, ms, _ = dev.ctx.pass_stats()
+                times[v].append(ms / n)
             if rep == 0:
                 h = hashlib.sha256()
                 st = dev.to_host()
@@ -43,7 +55,8 @@ def main():
                     h.update(getattr(st, f).tobytes())
                 digests[v] = h.hexdigest()[:16]
             dev.close()
-    out = {str(v): {"pass_ms": [round(t, 4) for t in times[v]],
+    key = "step_ms" if a.call else "pass_ms"
+    out = {str(v): {key: [round(t, 4) for t in times[v]],
                     "mean": round(sum(times[v]) / len(times[v]), 4)} for v in vals}
     out["bitwise_equal"] = len(set(digests.values())) == 1
     print(json.dumps({"knob": a.knob, "N": a.N, **out}))
