@@ -249,7 +249,8 @@ def test_shared_reciprocal_division():
     assert bad.value == 0
 
 
-@pytest.mark.parametrize("variant,xc", [(1, 0), (1, 3), (1, 128), (0, 8), (2, 5), (3, 0), (4, 0), (5, 3), (4, 16)])
+@pytest.mark.parametrize("variant,xc", [(1, 0), (1, 1), (1, 2), (1, 3), (1, 128), (0, 8), (2, 5), (3, 0),
+                                        (4, 0), (5, 3), (4, 16)])
 def test_march_kernel_matches_simple_kernel(variant, xc):
     """3-D marching (TMA ring) kernel == simple per-point kernel, bitwise, for
     every tile variant and several work-unit sizes (incl. a non-divisor)."""
@@ -266,6 +267,30 @@ def test_march_kernel_matches_simple_kernel(variant, xc):
         dev.close()
     assert_bitwise(outs[0][0], outs[1][0])
     np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-13)
+
+
+@pytest.mark.parametrize("xc", [0, 1, 5])
+def test_march_own_tile_store_modes_are_bitwise(xc):
+    """The march pass's own-tile write -- per-thread stores (tma_store 0), one
+    TMA bulk store (1), bulk store with L2 evict-first (2, the default) --
+    gives identical fields and records, incl. one-plane work units (every
+    plane is a unit start: all three other-colour planes are waited for)."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    outs = []
+    for mode in (0, 1, 2):
+        dev = kgs.DeviceFieldState.from_host(s0, g)
+        dev.ctx.set_tuning(march_planes=xc)
+        dev.ctx.set_param("tma_store", mode)
+        terms, bad = dev.ctx.step_dpavf2(args, 4, 0, 2)
+        outs.append((dev.to_host(), terms, bad))
+        dev.close()
+    for st, terms, bad in outs[1:]:
+        assert bad == outs[0][2] == 0
+        assert_bitwise(st, outs[0][0])
+        assert np.array_equal(terms, outs[0][1])
 
 
 def test_step_at_a_time_with_deferred_tail_is_bitwise(golden):
