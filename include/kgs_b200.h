@@ -206,7 +206,9 @@ double kgs_last_step_ms(kgs_ctx* ctx);
  * blocks per SM (0: occupancy maximum), planes per work unit of the 3-D
  * marching kernel (0: automatic, < 0: never use the marching kernel), and
  * the marching kernel's tile variant (0: 4x64, 1: 8x64, 2: 16x32, 3: 32x32
- * rows x slots; < 0: keep).  Results do not depend on these (bitwise). */
+ * rows x slots; 4, 5: 4x64 in clusters of 8 / 4 CTAs; 6: 4x64 with a
+ * producer warp and per-slot release barriers instead of a block barrier
+ * per plane; < 0: keep).  Results do not depend on these (bitwise). */
 int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
                    int march_planes, int march_variant);
 

@@ -4,6 +4,8 @@
 
 namespace {
 
+constexpr int kMarchVariantSlots = 7;   // march kernel variants (kgs_launch.cuh MV0..MV6)
+
 thread_local std::string g_last_error = "no error";
 
 // ---- NCCL, loaded lazily so single-GPU use never needs it --------------
@@ -56,12 +58,12 @@ struct Slab {
   int nx = 0;      // planes
   double* buf[2] = {nullptr, nullptr};    // colour c, ghost plane -1
   double* plane0[2] = {nullptr, nullptr}; // colour c, element (x=0,f=0,y=0,k=0)
-  MarchMaps maps[6][2];  // [march variant][colour]: TMA descriptors
-  bool has_tmaps[6] = {};  // variant fits this geometry
+  MarchMaps maps[kMarchVariantSlots][2];  // [march variant][colour]: TMA descriptors
+  bool has_tmaps[kMarchVariantSlots] = {};  // variant fits this geometry
   // fused steps (ping-pong): the other buffer set and its descriptors
   double* alt[2] = {nullptr, nullptr};
   double* alt0[2] = {nullptr, nullptr};
-  MarchMaps amaps[6][2];
+  MarchMaps amaps[kMarchVariantSlots][2];
   StepMaps smap[2];        // red of [0] the current set, [1] the other set
   bool has_smap = false;
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS

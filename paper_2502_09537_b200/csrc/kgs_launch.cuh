@@ -70,10 +70,11 @@ EncodeTiledFn encode_tiled() {
 
 // 3-D march kernel variants: tile rows x slots, ring depths, min blocks/SM.
 // Larger tile cross-sections re-read fewer halo rows/slots.
-template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_, int CL_ = 1>
+template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_, int CL_ = 1, bool PW_ = false>
 struct MarchVariant {
   static constexpr int TY = TY_, TK = TK_, NOTH = NOTH_, NOWN = NOWN_, MINB = MINB_, CL = CL_;
-  static constexpr int NT = TY * TK;
+  static constexpr bool PW = PW_;
+  static constexpr int NT = TY * TK + (PW ? 32 : 0);   // + the producer warp
   using L = MarchSmem<TY, TK, NOTH, NOWN>;
 };
 using MV0 = MarchVariant<4, 64, 4, 2, 4>;     // 256 threads, 4 blocks/SM
@@ -82,10 +83,14 @@ using MV2 = MarchVariant<16, 32, 4, 2, 2>;    // 512 threads, 2 blocks/SM
 using MV3 = MarchVariant<32, 32, 4, 2, 1>;    // 1024 threads, 1 block/SM
 using MV4 = MarchVariant<4, 64, 4, 2, 4, 8>;  // MV0 in clusters of 8 along y
 using MV5 = MarchVariant<4, 64, 4, 2, 4, 4>;  // MV0 in clusters of 4 along y
-constexpr int kMarchVariants = 6;
-constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY, MV4::TY, MV5::TY};
-constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK, MV4::TK, MV5::TK};
-constexpr int kVarCL[kMarchVariants] = {MV0::CL, MV1::CL, MV2::CL, MV3::CL, MV4::CL, MV5::CL};
+using MV6 = MarchVariant<4, 64, 4, 2, 4, 1, true>;  // MV0 + a producer warp, no block barrier
+constexpr int kMarchVariants = kMarchVariantSlots;
+constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY, MV4::TY, MV5::TY,
+                                        MV6::TY};
+constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK, MV4::TK, MV5::TK,
+                                        MV6::TK};
+constexpr int kVarCL[kMarchVariants] = {MV0::CL, MV1::CL, MV2::CL, MV3::CL, MV4::CL, MV5::CL,
+                                        MV6::CL};
 
 // L2 sector promotion of the TMA boxes.  The two-slot halo columns are 16 B
 // inside a neighbouring tile's lines: promoting them to 256-B fetches would
@@ -102,7 +107,8 @@ CUtensorMapL2promotion promo(int v) {
 // 4-D view of one colour array with dims ordered (slot, field, row, plane)
 // -- strides 8, pp*8, nk*8, ps*8 bytes -- so that a box lands in shared
 // memory as [row][field][slot] (MarchSmem); per variant four box shapes.
-int make_maps_for(kgs_ctx* ctx, Slab& s, double* const bufs[2], MarchMaps (&maps)[6][2]) {
+int make_maps_for(kgs_ctx* ctx, Slab& s, double* const bufs[2],
+                  MarchMaps (&maps)[kMarchVariantSlots][2]) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return fail(ctx, KGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {(cuuint64_t)ctx->nk, 4, (cuuint64_t)ctx->ny,
@@ -183,7 +189,8 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   using L = typename Var::L;
   constexpr int CL = Var::CL;
   auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
-                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG, CL>;
+                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG, CL,
+                         Var::PW>;
   static int occ = 0;  // resident CTAs per SM (or clusters per GPU / nsm when CL > 1)
   static int max_clusters = 0;
   if (occ == 0) {
@@ -470,7 +477,8 @@ int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, 
     case 2: return launch_march<MV2, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
     case 3: return launch_march<MV3, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
     case 4: return launch_march<MV4, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    default: return launch_march<MV5, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case 5: return launch_march<MV5, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    default: return launch_march<MV6, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
   }
 }
 

@@ -250,7 +250,7 @@ def test_shared_reciprocal_division():
 
 
 @pytest.mark.parametrize("variant,xc", [(1, 0), (1, 1), (1, 2), (1, 3), (1, 128), (0, 8), (2, 5), (3, 0),
-                                        (4, 0), (5, 3), (4, 16)])
+                                        (4, 0), (5, 3), (4, 16), (6, 0), (6, 1), (6, 5)])
 def test_march_kernel_matches_simple_kernel(variant, xc):
     """3-D marching (TMA ring) kernel == simple per-point kernel, bitwise, for
     every tile variant and several work-unit sizes (incl. a non-divisor)."""
