@@ -5,20 +5,28 @@
 
 Workload (BASELINE.json configs[3], the metric's named config): 3-D
 ellipsoids3d on a 1024^3 fp64 periodic grid, tau = 0.01.  A "step" is one
-DP-AVF2 time step = 2 * N^3 point-updates.  Inputs are
-generated on the device (synthetic, the reference's ellipsoids3d formulas);
-the 32 GiB state is far larger than the 126 MB L2, so no flush is needed.
+DP-AVF2 time step = 2 * N^3 point-updates.  Inputs are the
+reference's own preset (scenarios.py:69-89) built on the host block-parallel
+(bitwise the reference's numpy build) and uploaded; the 32 GiB state is far
+larger than the 126 MB L2, so no flush is needed.
+tests/test_gpu_headline.py checks this exact workload and call pattern bit
+for bit against the table-free C restatement of the reference.
 
-ours:       value = all ranks' point-updates / max-over-ranks device time of K
-            fused steps (CUDA events on the library's stream); e2e = the same
-            metric through the public API integrate() on a pinned host
-            FieldState (upload, K steps, download inside the timed region).
-reference:  the reference's CPU algorithm (oracle/ port: neighbour table,
-            colour lanes, phased threads) on all host cores, on a bounded
-            256^3 sample of the same scenario; rank 0 only.
-Multi-GPU (torchrun): slab decomposition along axis 0, NCCL halos; strong
-scaling at 1024^3 by default (--scaling weak: N = 1024 * cbrt(G) when G is
-a cube, else strong).
+ours:       value = all GPUs' point-updates / max-over-ranks device time of K
+            fused steps (CUDA events on the library's streams); e2e = the
+            same metric through the public API integrate() on the page-locked
+            host FieldState (upload, K steps, download inside the timed
+            region); cpu_baseline = the reference itself (dpavf from
+            baseline/_ref, numba, all host cores) on a 256^3 sample, the C
+            port beside it.
+reference:  the unmodified reference (baseline/_ref: dpavf.step_dpavf2,
+            checkerboard_schedule, PhasedExecutor over all host cores, as its
+            run_bench) on a bounded 512^3 sample; rank 0 only.
+GPUs:       --gpus N without a launcher drives GPUs 0..N-1 from one process
+            (one slab per GPU, halos stored into the neighbours' ghost
+            planes over NVLink); under torchrun one rank per GPU with NCCL
+            halos.  Strong scaling at 1024^3 by default; --scaling weak keeps
+            ~1024^3 points per GPU (2048^3 on 8 GPUs).
 """
 from __future__ import annotations
 
@@ -115,16 +123,62 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup(gpus: int):
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+class Launch:
+    """Who this process is and which GPUs it drives.
+
+    torchrun (WORLD_SIZE > 1): one rank per GPU, slab ``rank`` on
+    ``cuda:LOCAL_RANK``, NCCL halos (DistributedExecutor).  Plain
+    ``python bench.py --gpus N`` (no launcher): ONE process drives GPUs
+    0..N-1, one slab each, halos stored straight into the neighbours' ghost
+    planes over NVLink (CudaExecutor).  Either way fewer
+    visible devices than requested is an error, never a silent fallback."""
+
+    def __init__(self, gpus: int):
         import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return rank, world, local
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        ndev = torch.cuda.device_count()
+        if self.world > 1:
+            if self.local >= ndev:
+                raise SystemExit(f"bench.py: rank {self.rank} needs cuda:{self.local}, "
+                                 f"only {ndev} devices visible")
+            os.environ.setdefault("NCCL_DEBUG", "WARN")
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.devices = (self.local,)
+            self.n_gpus = self.world
+            self.mode = "torchrun+nccl"
+        else:
+            if gpus > ndev:
+                raise SystemExit(f"bench.py --gpus {gpus}: only {ndev} CUDA devices visible")
+            self.devices = tuple(range(max(gpus, 1)))
+            self.n_gpus = len(self.devices)
+            self.mode = "single-process" + ("+peer-stores" if self.n_gpus > 1 else "")
+        self.host_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+
+    def executor(self):
+        import paper_2502_09537_b200 as kgs
+        if self.world > 1:
+            return kgs.DistributedExecutor(self.rank, self.world, self.local)
+        return kgs.CudaExecutor(self.devices)
+
+    def describe(self) -> list:
+        """The GPUs actually used (all ranks), for the JSON line."""
+        import torch
+        mine = []
+        for d in self.devices:
+            pr = torch.cuda.get_device_properties(d)
+            mine.append({"rank": self.rank, "device": d, "name": pr.name,
+                         "pci_bus_id": getattr(pr, "pci_bus_id", None),
+                         "uuid": str(getattr(pr, "uuid", ""))})
+        if self.world > 1:
+            import torch.distributed as dist
+            out = [None] * self.world
+            dist.all_gather_object(out, mine)
+            mine = [x for r in out for x in r]
+        return mine
 
 
 def barrier(world: int):
@@ -143,18 +197,68 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def grid_n(args, world: int) -> int:
-    if args.scaling == "weak":
-        c = round(world ** (1 / 3))
-        if c ** 3 == world:
-            return args.N * c
-    return args.N
+def weak_n(base: int, gpus: int) -> int:
+    """Grid edge with ~base^3 points per GPU: base * cbrt(G) rounded to a
+    multiple of 128 (the march kernel's tile) that G divides -- exact for
+    cube G (8 GPUs: 2048^3, BASELINE configs[4])."""
+    target = base * gpus ** (1.0 / 3.0)
+    n = max(128, int(round(target / 128.0)) * 128)
+    while n % gpus:
+        n += 128
+    return n
+
+
+def grid_n(args, gpus: int) -> int:
+    return weak_n(args.N, gpus) if args.scaling == "weak" else args.N
 
 
 # --------------------------------------------------------------------------
-def cpu_baseline(steps: int, warmup: int, N: int = 256) -> dict:
-    """Reference CPU algorithm (oracle port) on all host threads, bounded
-    sample: N^3 ellipsoids3d, `steps` DP-AVF2 steps after `warmup`."""
+REF_SITE = ROOT / "baseline" / "_ref"
+
+
+def reference_cpu(steps: int, warmup: int, N: int) -> dict:
+    """The reference's own CPU path, unmodified: ``dpavf`` installed into
+    baseline/_ref, ``step_dpavf2`` with the checkerboard
+    schedule and a ``PhasedExecutor`` over all host cores, timed exactly as
+    its ``run_bench`` does (dpavf/harness.py:183-224: state, schedule and
+    JIT warm-up untimed), on the bench's scenario at N^3."""
+    if not (REF_SITE / "dpavf").is_dir():
+        raise FileNotFoundError(f"reference not installed in {REF_SITE}")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/kgs_numba_cache")
+    if str(REF_SITE) not in sys.path:
+        sys.path.insert(0, str(REF_SITE))
+    import dpavf
+    from dpavf.harness import make_schedule
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    sc = dpavf.get_scenario(SCENARIO)
+    g = sc.default_grid(N)
+    st = sc.state(g)
+    sched = make_schedule("checkerboard", g, workers=threads)
+    coeffs = dpavf.precompute_coefficients(sc.params, TAU / 2.0, g)
+    ex = dpavf.PhasedExecutor(threads) if threads > 1 else dpavf.SerialExecutor()
+    setup = time.perf_counter() - t0
+    try:
+        for _ in range(max(warmup, 1)):
+            dpavf.step_dpavf2(st, sched, coeffs, ex, g)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            dpavf.step_dpavf2(st, sched, coeffs, ex, g)
+        dt = time.perf_counter() - t0
+    finally:
+        ex.close()
+    return {"value": 2.0 * g.M * steps / dt, "unit": UNIT, "cores": threads,
+            "kind": "reference",
+            "sample": f"{N}^3 {SCENARIO}, {steps} DP-AVF2 steps after {max(warmup, 1)} warm-up "
+                      f"(incl. numba JIT), dpavf.step_dpavf2 + checkerboard_schedule + "
+                      f"PhasedExecutor({threads}) from baseline/_ref (unmodified reference)",
+            "seconds": dt, "setup_s": setup, "N": N,
+            "numba": __import__("numba").__version__}
+
+
+def port_cpu(steps: int, warmup: int, N: int = 256) -> dict:
+    """The C restatement of the same algorithm (oracle/, "port"), all host
+    threads -- reported beside the reference as a cross-check."""
     import oracle
     import paper_2502_09537_b200 as kgs
     sc = kgs.get_scenario(SCENARIO)
@@ -174,55 +278,119 @@ def cpu_baseline(steps: int, warmup: int, N: int = 256) -> dict:
             "seconds": dt}
 
 
+def cpu_baseline(steps: int = 3, warmup: int = 1, N: int = 256) -> dict:
+    """cpu_baseline for our arm's line: the reference itself on a bounded
+    sample (port as a secondary field; the port alone if the reference
+    cannot run here)."""
+    port = port_cpu(steps, warmup, N)
+    keys = ("value", "unit", "cores", "kind", "sample")
+    try:
+        ref = reference_cpu(steps, warmup, N)
+    except Exception as e:  # noqa: BLE001 - reported, not hidden
+        out = {k: port[k] for k in keys}
+        out["reference_error"] = f"{type(e).__name__}: {e}"
+        return out
+    out = {k: ref[k] for k in keys}
+    out["port"] = {k: port[k] for k in keys}
+    return out
+
+
 def run_reference(args):
-    rank, world, _ = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
+    """--impl reference: the reference's CPU path on the host cores (rank 0
+    only under torchrun; other ranks exit without work)."""
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    N = grid_n(args, world)
-    steps = max(1, min(args.steps, 40))
-    cb = cpu_baseline(steps, args.warmup)
+    n_gpus = world if world > 1 else max(args.gpus, 1)
+    N = grid_n(args, n_gpus)
+    # bounded sample of the workload: 512^3 (1/8 of the 1024^3 grid; time is
+    # linear in N^d, PAPER.md:1803), capped so the run ends in minutes
+    ns = min(N, args.ref_N)
+    steps = max(1, min(args.steps, 20))
+    warm = max(1, min(args.warmup, 2))
+    cb = reference_cpu(steps, warm, ns)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "n_gpus": n_gpus, "steps": steps, "warmup": warm,
         "ms_per_step": 1e3 * cb["seconds"] / steps,
         "higher_is_better": True,
-        "scaling": "weak" if (args.scaling == "weak" and round(world ** (1 / 3)) ** 3 == world)
-                   else "strong",
+        "scaling": "weak" if args.scaling == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"3D KGS {SCENARIO} N={N}^3 fp64, tau={TAU}, checkerboard DP-AVF2",
-                   "sample": cb["sample"]},
+                   "sample": cb["sample"], "sample_N": ns},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "setup_s": cb["setup_s"], "numba": cb["numba"],
     }
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------
+def host_preset(g, L: "Launch", pinned: bool):
+    """The reference's ellipsoids3d preset (scenarios.py:69-89) on this
+    process's planes, built block-parallel on the host (bitwise the
+    reference's numpy build), in page-locked memory when ``pinned``."""
+    import paper_2502_09537_b200 as kgs
+    from paper_2502_09537_b200.device import pinned_empty, slab_range
+    from paper_2502_09537_b200.scenarios import build_preset
+    if L.world > 1:
+        x0, nx = slab_range(g.N, L.rank, L.world)
+        planes, n = (x0, x0 + nx), nx * g.N * g.N
+    else:
+        planes, n = None, g.M
+    alloc = pinned_empty if pinned else np.empty
+    out = kgs.FieldState(*(alloc(n) for _ in range(4)), 0.0)
+    # the local ranks of one host share its cores
+    workers = max(1, (os.cpu_count() or 1) // max(L.host_ranks, 1))
+    return build_preset(SCENARIO, g, out=out, planes=planes, workers=workers)
+
+
+def host_memory_ok(nbytes: int, L: "Launch") -> bool:
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        return True
+    return nbytes * max(L.host_ranks, 1) * 1.15 < avail
+
+
 def run_ours(args):
     import torch
     import paper_2502_09537_b200 as kgs
 
-    rank, world, local = dist_setup(args.gpus)
-    N = grid_n(args, world)
+    L = Launch(args.gpus)
+    world = L.world
+    N = grid_n(args, L.n_gpus)
     sc = kgs.get_scenario(SCENARIO)
     g = sc.default_grid(N)
-    ex = kgs.DistributedExecutor(rank, world, local) if world > 1 else kgs.CudaExecutor((local,))
+    ex = L.executor()
     sch = kgs.checkerboard_schedule(g)
     coeffs = kgs.precompute_coefficients(sc.params, TAU / 2.0, g)
     kargs = coeffs.kernel_args()
     K, W = args.steps, args.warmup
 
-    dev = kgs.DeviceFieldState.from_preset(SCENARIO, g, ex)
+    # inputs: the reference's host preset, uploaded (bitwise scenarios.py);
+    # kept on the host (page-locked) as the e2e input
+    local_bytes = 32 * g.M // max(world, 1)
+    t_in = time.perf_counter()
+    host = None
+    if host_memory_ok(local_bytes, L):
+        host = host_preset(g, L, pinned=not args.no_e2e)
+        dev = kgs.DeviceFieldState.from_host(host, g, ex)
+        inputs = "host preset (block-parallel numpy, bitwise reference scenarios.py:69-89)"
+    else:   # too little host memory for a host copy: same formulas on the device
+        dev = kgs.DeviceFieldState.from_preset(SCENARIO, g, ex)
+        inputs = "device preset (kgs_fill_preset; host memory too small for a host copy)"
+    t_in = time.perf_counter() - t_in
     ctx = dev.ctx
-    points_local = ctx.points
     # warm-up (untimed)
     ctx.step_dpavf2(kargs, W, 0, 0)
     barrier(world)
     torch.cuda.synchronize()
     l0 = ctx.launch_count()
     ctx.pass_timing(True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(L.devices[0]) as clk:
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -247,7 +415,7 @@ def run_ours(args):
     achieved = BYTES_PER_UPDATE * upd_per_launch / (avg_pass_ms / 1e3) / 1e9
     nc = ncu_traffic()
     traffic = None
-    if nc and nc.get("N") == N and nc.get("world") == world:
+    if nc and nc.get("N") == N and nc.get("world") == L.n_gpus:
         traffic = nc.get("dram_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
@@ -283,18 +451,12 @@ def run_ours(args):
             "max_rel_mass_change": max(abs(m - em[0][1]) / abs(em[0][1]) for _, m in em),
             "note": "energy is the scheme's invariant (round-off drift); mass is not conserved "
                     "by DP-AVF2 and drifts at the reference's own rate (grows with N)"}
+    dev.close()
+    del dev
 
-    # e2e through the public API: integrate() on a pinned host state
+    # e2e through the public API: integrate() on the host state
     e2e = None
-    if not args.no_e2e:
-        if world == 1:
-            host = kgs.FieldState.pinned(g)
-        else:   # each rank holds only its own slab on the host (32 GiB / world)
-            from paper_2502_09537_b200.device import pinned_empty
-            host = kgs.FieldState(*(pinned_empty(points_local) for _ in range(4)), 0.0)
-        dev.download(host)
-        dev.close()
-        del dev
+    if not args.no_e2e and host is not None:
         # untimed warm-up call (W steps): creates the cached context and its
         # pipeline buffers, as the device timing's warm-up steps do
         kgs.integrate(host, g, sc.params, sch, ex, TAU, W * TAU, record_stride=W)
@@ -304,34 +466,35 @@ def run_ours(args):
         kgs.integrate(host, g, sc.params, sch, ex, TAU, K * TAU, record_stride=K)
         torch.cuda.synchronize()
         e2e_wall = max_over_ranks(time.perf_counter() - t0, world)
-        state_bytes = 4 * 8 * g.M // world
         e2e = {"value": updates / e2e_wall, "unit": UNIT,
-               "h2d_bytes_per_step": state_bytes // K, "d2h_bytes_per_step": state_bytes // K,
+               "h2d_bytes_per_step": local_bytes * world // K,
+               "d2h_bytes_per_step": local_bytes * world // K,
                "wall_s": e2e_wall, "steps_per_call": K,
-               "note": "integrate(host pinned FieldState): upload + K steps + download in one "
-                       "call (pipelined: chunks stream in, passes follow as a wavefront, "
-                       "finished chunks stream out); one untimed warm-up call first"}
+               "note": "integrate(host page-locked FieldState): upload + K steps + download in "
+                       "one call (pipelined on one slab: chunks stream in, passes follow as a "
+                       "wavefront, finished chunks stream out); one untimed warm-up call first"}
         kgs.clear_contexts()
-    else:
-        dev.close()
+    gpus_used = L.describe()
+    barrier(world)
 
-    if rank != 0:
+    if L.rank != 0:
         return
     cb = None
-    if world == 1 and not args.no_cpu:
-        cb = cpu_baseline(min(K, 10), 1)
-        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if not args.no_cpu:
+        # after every GPU timing (rank 0 alone; no other rank is still working)
+        cb = cpu_baseline(3, 1, 256)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": L.n_gpus, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
-        # weak: per-GPU work fixed (N = 1024 * cbrt(G) for cube G, incl. G = 1)
-        "scaling": "weak" if (args.scaling == "weak" and round(world ** (1 / 3)) ** 3 == world)
-                   else "strong",
+        "scaling": "weak" if args.scaling == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"3D KGS {SCENARIO} N={N}^3 fp64, tau={TAU}, checkerboard DP-AVF2",
                    "grid_points": g.M, "updates_per_step": 2 * g.M,
-                   "parallelism": f"slab{world}", "l2": "inputs (32 GiB state) >> L2 (126 MB)",
-                   "record_stride": K},
+                   "points_per_gpu": g.M // L.n_gpus,
+                   "parallelism": f"slab{L.n_gpus} ({L.mode})",
+                   "l2": "inputs (32 GiB state) >> L2 (126 MB)",
+                   "record_stride": K, "inputs": inputs, "input_build_s": t_in},
+        "gpus": gpus_used,
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
         "diagnostics": diag,
         "clocks": clk.summary(), "wall_s": wall, "energy_final": e,
@@ -350,6 +513,8 @@ def main():
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-N", type=int, default=512,
+                    help="--impl reference: grid edge of the bounded CPU sample")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -59,6 +59,9 @@ def lib() -> ctypes.CDLL:
         L.orc_step_dpavf2.argtypes = [P, P, P, P, P, ctypes.c_int, P, I64, P, I64, P, I64,
                                       ctypes.c_int]
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_free_sweep.argtypes = [ctypes.c_int, I64, P, P, P, P, ctypes.c_int, P]
+        L.orc_free_step_dpavf2.argtypes = [ctypes.c_int, I64, P, P, P, P, P, I64]
+        L.orc_energy_row_terms.argtypes = [ctypes.c_int, I64, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -110,6 +113,42 @@ class CheckerboardOracle:
         lib().orc_step_dpavf2(*map(_p, f), _p(self.nbrs), self.nn, _p(self.red),
                               self.red.shape[0], _p(self.black), self.black.shape[0],
                               _p(c), nsteps, workers)
+
+
+class TableFreeOracle:
+    """The same restatement without the (M, 2d) neighbour table or index
+    lists: periodic neighbours computed from coordinates, rows in parallel
+    (kgs_oracle.c, ``orc_free_*``).  For grids whose table does not fit in
+    host memory -- the 1024^3 headline config (tests/test_gpu_headline.py).
+    Pinned to the golden vectors like ``CheckerboardOracle``."""
+
+    def __init__(self, d: int, N: int):
+        if N % 2:
+            raise ValueError("checkerboard needs even N")
+        self.d, self.N, self.M = d, N, N**d
+
+    def _fields(self, state):
+        f = [state.P, state.Q, state.U, state.V]
+        for a in f:
+            assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"] and a.shape == (self.M,)
+        return f
+
+    def sweep(self, state, kernel_args, adjoint: bool) -> None:
+        c = np.asarray(kernel_args, dtype=np.float64)
+        lib().orc_free_sweep(self.d, self.N, *map(_p, self._fields(state)), int(adjoint), _p(c))
+
+    def step_dpavf2(self, state, kernel_args, nsteps: int = 1) -> None:
+        c = np.asarray(kernel_args, dtype=np.float64)
+        lib().orc_free_step_dpavf2(self.d, self.N, *map(_p, self._fields(state)), _p(c), nsteps)
+
+    def energy_terms(self, state) -> np.ndarray:
+        """The 8 unscaled sums (as ``energy_terms`` below): per-row partials
+        in C, rows summed exactly."""
+        import math
+        rows = (self.N**(self.d - 1)) if self.d > 1 else 1
+        part = np.empty((rows, 8))
+        lib().orc_energy_row_terms(self.d, self.N, *map(_p, self._fields(state)), _p(part))
+        return np.array([math.fsum(part[:, k]) for k in range(8)])
 
 
 # ---------------------------------------------------------------------------

@@ -150,6 +150,138 @@ void orc_step_dpavf2(double* P, double* Q, double* U, double* V,
   }
 }
 
+/* ------------------------------------------------------------------------
+ * Table-free restatement for grids whose neighbour table does not fit in
+ * host memory (1024^3: the table alone is 48 GiB, grid.py:54-64).  Same
+ * per-point arithmetic as sweep_lane (kernels.py:43-54, 83-94), same
+ * neighbour summation order (-x,+x,-y,+y,-z,+z; kernels.py:35-42) with the
+ * periodic neighbours computed from coordinates, same colour convention
+ * (red = index-sum parity 1, ordering.py:125-128) and the same phase order
+ * as orc_step_dpavf2.  Inside a colour phase every update reads only
+ * other-colour values, so the visiting order (here: rows in parallel) is
+ * immaterial -- the bitwise-equality tests against the golden vectors pin
+ * this.  The natural index is i = x*N^2 + y*N + z; axes of size 1 (the
+ * missing leading axes of d = 1, 2) are skipped.
+ * ---------------------------------------------------------------------- */
+static void free_phase(int d, int64_t N, double* P, double* Q, double* U,
+                       double* V, int colour, int adjoint, const double* c) {
+  const double alpha = c[0], beta = c[1], gcoef = c[2], c_uv = c[3],
+               uv_nbr = c[4], gU = c[5], half_tau = c[6], i00 = c[7],
+               i01 = c[8], i10 = c[9], i11 = c[10];
+  const int64_t nx = d >= 3 ? N : 1, ny = d >= 2 ? N : 1, nz = N;
+  const int64_t sx = ny * nz, sy = nz;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t x = 0; x < nx; ++x) {
+    for (int64_t y = 0; y < ny; ++y) {
+      const int64_t xm = x == 0 ? nx - 1 : x - 1, xp = x == nx - 1 ? 0 : x + 1;
+      const int64_t ym = y == 0 ? ny - 1 : y - 1, yp = y == ny - 1 ? 0 : y + 1;
+      const int64_t row = x * sx + y * sy;
+      const int64_t rxm = xm * sx + y * sy, rxp = xp * sx + y * sy;
+      const int64_t rym = x * sx + ym * sy, ryp = x * sx + yp * sy;
+      for (int64_t z = (colour + x + y) & 1; z < nz; z += 2) {
+        const int64_t zm = z == 0 ? nz - 1 : z - 1, zp = z == nz - 1 ? 0 : z + 1;
+        const int64_t i = row + z;
+        int64_t nb[6];
+        int nn = 0;
+        if (nx > 1) { nb[nn++] = rxm + z; nb[nn++] = rxp + z; }
+        if (ny > 1) { nb[nn++] = rym + z; nb[nn++] = ryp + z; }
+        nb[nn++] = row + zm;
+        nb[nn++] = row + zp;
+        double SP = 0.0, SQ = 0.0, SU = 0.0;
+        for (int k = 0; k < nn; ++k) {
+          SP += P[nb[k]];
+          SQ += Q[nb[k]];
+          SU += U[nb[k]];
+        }
+        const double Pi = P[i], Qi = Q[i], Ui = U[i], Vi = V[i];
+        if (!adjoint) { /* kernels.py:43-54 */
+          const double cr = gcoef * Ui - alpha;
+          const double rr = -cr * Pi - Qi - beta * SP;
+          const double ri = Pi - cr * Qi - beta * SQ;
+          const double den = cr * cr + 1.0;
+          const double Pn = (rr * cr + ri) / den;
+          const double Qn = (ri * cr - rr) / den;
+          P[i] = Pn;
+          Q[i] = Qn;
+          const double r1 = Ui + half_tau * Vi;
+          const double r2 = Vi - c_uv * Ui + uv_nbr * SU + gU * (Pn * Pn + Qn * Qn);
+          U[i] = i00 * r1 + i01 * r2;
+          V[i] = i10 * r1 + i11 * r2;
+        } else { /* kernels.py:83-94 */
+          const double r1 = Ui + half_tau * Vi;
+          const double r2 = Vi - c_uv * Ui + uv_nbr * SU + gU * (Pi * Pi + Qi * Qi);
+          const double Un = i00 * r1 + i01 * r2;
+          const double Vn = i10 * r1 + i11 * r2;
+          U[i] = Un;
+          V[i] = Vn;
+          const double cr = gcoef * Un - alpha;
+          const double rr = -cr * Pi - Qi - beta * SP;
+          const double ri = Pi - cr * Qi - beta * SQ;
+          const double den = cr * cr + 1.0;
+          P[i] = (rr * cr + ri) / den;
+          Q[i] = (ri * cr - rr) / den;
+        }
+      }
+    }
+  }
+}
+
+/* One checkerboard sweep: base = red then black (step_base,
+ * integrator.py:107-112), adjoint = black then red (step_adjoint on the
+ * reversed schedule, :115-121, ordering.py:139-149). */
+void orc_free_sweep(int d, int64_t N, double* P, double* Q, double* U,
+                    double* V, int adjoint, const double* c) {
+  free_phase(d, N, P, Q, U, V, adjoint ? 0 : 1, adjoint, c);
+  free_phase(d, N, P, Q, U, V, adjoint ? 1 : 0, adjoint, c);
+}
+
+/* nsteps of step_dpavf2 (integrator.py:124-129), table-free. */
+void orc_free_step_dpavf2(int d, int64_t N, double* P, double* Q, double* U,
+                          double* V, const double* c, int64_t nsteps) {
+  for (int64_t s = 0; s < nsteps; ++s) {
+    orc_free_sweep(d, N, P, Q, U, V, 0, c);
+    orc_free_sweep(d, N, P, Q, U, V, 1, c);
+  }
+}
+
+/* The 8 unscaled energy sums of include/kgs_b200.h (grid.py:152-187
+ * before the h-scaling), one partial per (x, y) row so the caller can sum
+ * the rows exactly (math.fsum): out[row*8 + t] for
+ *   t = 0..2: sum over axes of (f[+axis] - f)^2 for f = P, Q, U
+ *           (np.roll(f, -1, axis) - f, grid.py:152-163)
+ *   t = 3: V.V, 4: U.U, 5: (P^2 + Q^2).U, 6: P.P, 7: Q.Q. */
+void orc_energy_row_terms(int d, int64_t N, const double* P, const double* Q,
+                          const double* U, const double* V, double* out) {
+  const int64_t nx = d >= 3 ? N : 1, ny = d >= 2 ? N : 1, nz = N;
+  const int64_t sx = ny * nz, sy = nz;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t x = 0; x < nx; ++x) {
+    for (int64_t y = 0; y < ny; ++y) {
+      const int64_t xp = x == nx - 1 ? 0 : x + 1, yp = y == ny - 1 ? 0 : y + 1;
+      const int64_t row = x * sx + y * sy;
+      const double* F[3] = {P, Q, U};
+      double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int64_t z = 0; z < nz; ++z) {
+        const int64_t i = row + z, zp = z == nz - 1 ? 0 : z + 1;
+        for (int q = 0; q < 3; ++q) {
+          const double f = F[q][i];
+          double a = 0.0;
+          if (nx > 1) { const double e = F[q][xp * sx + y * sy + z] - f; a += e * e; }
+          if (ny > 1) { const double e = F[q][x * sx + yp * sy + z] - f; a += e * e; }
+          { const double e = F[q][row + zp] - f; a += e * e; }
+          t[q] += a;
+        }
+        t[3] += V[i] * V[i];
+        t[4] += U[i] * U[i];
+        t[5] += (P[i] * P[i] + Q[i] * Q[i]) * U[i];
+        t[6] += P[i] * P[i];
+        t[7] += Q[i] * Q[i];
+      }
+      for (int k = 0; k < 8; ++k) out[(x * ny + y) * 8 + k] = t[k];
+    }
+  }
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

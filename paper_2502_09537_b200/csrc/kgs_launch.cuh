@@ -4,6 +4,17 @@
 
 namespace {
 
+// Function attributes (the dynamic shared-memory opt-in) and occupancy are
+// per device context: every per-kernel cache below is indexed by the
+// current device, so a context whose slabs sit on several GPUs configures
+// each of them (the launches set the slab's device first).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+
 // ---- kernel dispatch -----------------------------------------------------
 // Launch a kernel that opens with griddepcontrol.wait / launch_dependents as
 // a programmatic dependent of the previous kernel on the stream (its launch
@@ -32,7 +43,8 @@ template <int D, int COL, int OP1, int OP2, bool DIAG, bool CHECK>
 int launch_t(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c,
              int step_no) {
   auto kern = colour_pass<D, COL, OP1, OP2, DIAG, CHECK>;
-  static int occ = 0;  // per instantiation; all devices are B200
+  static int occ_dev[kMaxDevices] = {};  // per instantiation and device
+  int& occ = occ_dev[current_device()];
   if (occ == 0) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
     if (occ < 1) occ = 1;
@@ -191,8 +203,12 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
                          DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG, CL,
                          Var::PW>;
-  static int occ = 0;  // resident CTAs per SM (or clusters per GPU / nsm when CL > 1)
-  static int max_clusters = 0;
+  // resident CTAs per SM (or clusters per GPU / nsm when CL > 1), per device
+  static int occ_dev[kMaxDevices] = {};
+  static int max_clusters_dev[kMaxDevices] = {};
+  const int dev = current_device();
+  int& occ = occ_dev[dev];
+  int& max_clusters = max_clusters_dev[dev];
   if (occ == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Var::NT, L::bytes));
@@ -267,7 +283,8 @@ bool resident_eligible(const kgs_ctx* ctx) {
 template <int D>
 int launch_resident_d(kgs_ctx* ctx, Slab& s, const Coeffs& c, const ResidentCfg& rc) {
   auto kern = resident_steps<D>;
-  static bool attr = false;
+  static bool attr_dev[kMaxDevices] = {};
+  bool& attr = attr_dev[current_device()];
   if (!attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kResidentMaxBytes));
@@ -358,7 +375,8 @@ template <bool DIAG, int K4OP2>
 int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int xb) {
   constexpr int NT = kStepTY * kStepTK;
   auto kern = step_pass<DIAG, K4OP2, kStepTY, kStepTK, 2>;
-  static int occ = 0;
+  static int occ_dev[kMaxDevices] = {};
+  int& occ = occ_dev[current_device()];
   if (occ == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)StepS::bytes));

@@ -89,13 +89,15 @@ class FieldState:
         return cls(np.zeros(M), np.zeros(M), np.zeros(M), np.zeros(M), 0.0)
 
     @classmethod
-    def pinned(cls, grid: GridSpec) -> "FieldState":
-        """Zero state whose arrays live in page-locked host memory (fast,
-        asynchronous host<->device copies; used for end-to-end timing)."""
+    def pinned(cls, grid: GridSpec, zero: bool = True) -> "FieldState":
+        """State whose arrays live in page-locked host memory (fast,
+        asynchronous host<->device copies; used for end-to-end timing);
+        zero-filled unless ``zero=False`` (the caller fills every value)."""
         from .device import pinned_empty
         f = [pinned_empty(grid.M) for _ in range(4)]
-        for a in f:
-            a.fill(0.0)
+        if zero:
+            for a in f:
+                a.fill(0.0)
         return cls(*f, 0.0)
 
     def copy(self) -> "FieldState":

@@ -315,3 +315,31 @@ def test_one_call_path_only_takes_whole_grid_writable_float64():
     f32 = kgs.FieldState.zeros(g)
     f32.P = np.zeros(g.M, dtype=np.float32)
     assert not _pipeline_ok(f32, g)
+
+
+@pytest.mark.parametrize("name,N,block", [("ellipsoids3d", 48, 1000), ("ellipsoids3d", 64, 1 << 22),
+                                          ("ellipsoids3d", 30, 7 * 900),
+                                          ("fourpeak2d", 256, 3000), ("gaussian2d", 128, 128 * 5)])
+def test_build_preset_blocks_bitwise(name, N, block):
+    """The block-parallel host build (bench.py, the 1024^3 parity test) is
+    bitwise the whole-grid preset, i.e. the reference's scenarios.py:40-89."""
+    from paper_2502_09537_b200.scenarios import build_preset
+    sc = kgs.get_scenario(name)
+    g = sc.default_grid(N)
+    whole = sc.state(g)
+    blocks = build_preset(name, g, block_points=block, workers=4)
+    for f in "PQUV":
+        assert np.array_equal(getattr(whole, f), getattr(blocks, f)), f
+
+
+def test_build_preset_slab_is_the_whole_grid_slice():
+    from paper_2502_09537_b200.scenarios import build_preset
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(32)
+    whole = sc.state(g)
+    for lo, hi in ((0, 8), (8, 16), (24, 32), (5, 13)):
+        slab = build_preset("ellipsoids3d", g, planes=(lo, hi), block_points=3000)
+        for f in "PQUV":
+            assert np.array_equal(getattr(slab, f), getattr(whole, f)[lo * 1024:hi * 1024])
+    with pytest.raises(ValueError):
+        build_preset("ellipsoids3d", g, planes=(0, 33))

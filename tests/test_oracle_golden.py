@@ -143,3 +143,41 @@ def test_c_oracle_tables_match_reference_conventions():
     parity = np.indices(g.shape).sum(axis=0).ravel() % 2
     assert np.array_equal(orc.red, np.nonzero(parity == 1)[0])
     assert np.array_equal(orc.black, np.nonzero(parity == 0)[0])
+
+
+# ---- the table-free restatement (checker for the 1024^3 headline config) --
+@pytest.mark.parametrize("name", run_names())
+def test_table_free_oracle_integrate_bitwise(golden, name):
+    c = golden.case(name)
+    s = c.state(0)
+    oracle.TableFreeOracle(c.grid.d, c.grid.N).step_dpavf2(s, c.kernel_args, c.meta["n_steps"])
+    assert_bitwise(s, c.state(1))
+
+
+@pytest.mark.parametrize("name", sweep_names())
+def test_table_free_oracle_single_sweeps_bitwise(golden, name):
+    c = golden.case(name)
+    s = c.state(0)
+    oracle.TableFreeOracle(c.grid.d, c.grid.N).sweep(s, c.kernel_args,
+                                                     c.meta["kind"] == "adjoint")
+    assert_bitwise(s, c.state(1))
+
+
+@pytest.mark.parametrize("d,N", [(3, 24), (2, 64), (1, 128), (3, 2)])
+def test_table_free_oracle_matches_table_oracle(d, N):
+    """Beyond the golden sizes: random state, 3 steps, both C restatements."""
+    g = GridSpec(d, -3.0, 3.0, N)
+    a = seeded_random_state(g, 77, 0.5)
+    b = a.copy()
+    args = oracle.kernel_args(PhysParams(-0.4, 0.1, 0.1, 0.2), 0.005, g)
+    oracle.TableFreeOracle(d, N).step_dpavf2(a, args, 3)
+    oracle.CheckerboardOracle(d, N).step_dpavf2(b, args, 3, workers=2)
+    assert_bitwise(a, b)
+
+
+@pytest.mark.parametrize("d,N", [(3, 16), (2, 64), (1, 256), (3, 2)])
+def test_table_free_energy_terms(d, N):
+    g = GridSpec(d, -3.0, 3.0, N)
+    s = seeded_random_state(g, 11, 0.5)
+    np.testing.assert_allclose(oracle.TableFreeOracle(d, N).energy_terms(s),
+                               oracle.energy_terms(s, g), rtol=1e-13, atol=0)
