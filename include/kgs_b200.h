@@ -136,6 +136,13 @@ int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c);
  * every other entry point applies a pending adjoint first, and the last
  * step is then not checked for finiteness (step_dpavf2 does not check). */
 #define KGS_STEP_DEFER_TAIL 1
+/* flags & KGS_STEP_BACKUP: first copy the state at step_offset (a pending
+ * tail applied) into the context's second buffer set (allocated on first
+ * use; skipped when it does not fit), so that after KGS_ENONFINITE the
+ * caller can kgs_restore_backup() and replay exactly to the first bad step
+ * -- integrate()'s contract that the state is left after that step
+ * (integrator.py:169-171).  Costs one device copy of the state. */
+#define KGS_STEP_BACKUP 8
 int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
                     int64_t step_offset, int64_t record_stride,
                     double* terms_out, int64_t* first_bad_step, int flags);
@@ -167,6 +174,30 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
  * number of events, -1 on bad arguments. */
 int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap);
 
+/* The pass program kgs_step_dpavf2 executes on every slab / rank of `nx`
+ * local planes (split = 1: several slabs or ranks, faces exchanged; 0: one
+ * slab, x wraps in the kernel) -- the same list, from the same function.
+ * Rows of 9 int64 (kind, col, op1, op2, diag, check, step, xa, xb) written to
+ * out[9 * i ..] (at most `cap` rows):
+ *   1 LAUNCH      colour `col` pass over local planes [xa, xb): op1 then op2
+ *                 (0 none, 1 base, 2 adjoint), energy terms (diag) after the
+ *                 adjoint, finiteness check (check) tagged with `step`
+ *   2 WAIT_XCH    wait until the pending halo exchange has landed
+ *   3 XCH         start the exchange of colour `col` faces: send P, Q, U of
+ *                 plane 0 to rank-1 and of plane nx-1 to rank+1, receive
+ *                 into ghost planes nx (from rank+1) and -1 (from rank-1)
+ *   4 RECORD      reduce the energy partials into record slot `step`
+ *   5 DEFER       the last red adjoint is left pending
+ *   6 PASS_BEGIN / 7 PASS_END   bracket one colour pass (xa = 1: timed)
+ * flags: KGS_STEP_DEFER_TAIL, KGS_PROGRAM_HEAD_FUSED (the previous call left
+ * its red adjoint pending with the same coefficients).  Mirrors
+ * integrator.py:167-179 (the DP-AVF2 loop) over dpavf/executor.py:60-71
+ * (phases separated by barriers; here by exchanges and stream events).
+ * Pure host logic; returns the number of rows, -1 on bad arguments. */
+#define KGS_PROGRAM_HEAD_FUSED 2
+int64_t kgs_step_program(int64_t nx, int split, int64_t nsteps, int64_t step_offset,
+                         int64_t record_stride, int flags, int64_t* out, int64_t cap);
+
 /* ---- diagnostics (dpavf/grid.py:152-187) ------------------------------- */
 
 /* Unscaled sums over this context's points, deterministic for a given
@@ -176,6 +207,11 @@ int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, in
  *   t[3] = V.V, t[4] = U.U, t[5] = (P^2+Q^2).U, t[6] = P.P, t[7] = Q.Q
  * discrete_energy = h^d * (0.5*(k1*(t0+t1)/h^2 + k2*t2/h^2 + t3 + mu^2*t4)
  *                          - gamma*t5),  mass = h^d * (t6 + t7). */
+/* Restore the state saved by the last kgs_step_dpavf2(..., KGS_STEP_BACKUP)
+ * call (KGS_EINVAL if there is none, or the state changed since through
+ * another entry point). */
+int kgs_restore_backup(kgs_ctx* ctx);
+
 int kgs_energy_terms(kgs_ctx* ctx, double* terms_out);
 
 /* discrete_energy(state, params, grid) and mass(state, grid) for the
@@ -275,6 +311,20 @@ int kgs_host_free(void* p);
 
 /* ABI version (major*100 + minor). */
 int kgs_abi_version(void);
+
+/* Build flags of this library: KGS_BUILD_EXPERIMENTAL (-DKGS_EXPERIMENTAL:
+ * the slower fused one-march step, march variants 4..6 and kgs_debug_pass,
+ * kept for the DESIGN.md §5 measurements) and KGS_BUILD_CHECKED
+ * (-DKGS_CHECKED: in-kernel index asserts).  The default library has
+ * neither. */
+/* CUDA devices visible to this process (cudaGetDeviceCount; 0 without a
+ * driver) -- ExecutorConfig("cuda", workers) uses one slab per GPU when
+ * workers <= this, virtual slabs on device 0 otherwise. */
+int kgs_device_count(void);
+
+#define KGS_BUILD_EXPERIMENTAL 1
+#define KGS_BUILD_CHECKED 2
+int kgs_build_flags(void);
 
 #ifdef __cplusplus
 }

@@ -23,15 +23,16 @@ KGS_ENONFINITE = -4
 KGS_ENOMEM = -5
 NTERMS = 8
 KGS_STEP_DEFER_TAIL = 1
+KGS_STEP_BACKUP = 8
 
 # Every symbol include/kgs_b200.h declares (checked by the CPU test suite).
 EXPORTED = (
     "kgs_create", "kgs_create_dist", "kgs_nccl_unique_id", "kgs_destroy",
     "kgs_local_range", "kgs_upload", "kgs_download", "kgs_sweep",
-    "kgs_step_dpavf2", "kgs_integrate_host", "kgs_pipeline_plan", "kgs_energy_terms",
+    "kgs_step_dpavf2", "kgs_integrate_host", "kgs_pipeline_plan", "kgs_step_program", "kgs_restore_backup", "kgs_energy_terms",
     "kgs_energy_mass",
     "kgs_all_finite", "kgs_last_error", "kgs_launch_count",
-    "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version",
+    "kgs_last_step_ms", "kgs_fill_preset", "kgs_abi_version", "kgs_build_flags", "kgs_device_count",
     "kgs_pass_timing", "kgs_pass_stats", "kgs_host_alloc", "kgs_host_free",
     "kgs_set_tuning", "kgs_selftest_division", "kgs_debug_pass",
     "kgs_set_promotion", "kgs_set_param", "kgs_upload_planes", "kgs_download_planes",
@@ -92,6 +93,9 @@ def load() -> ctypes.CDLL:
                                               _I64, _I64, _I64, _DP, _DP,
                                               ctypes.POINTER(_I64), ctypes.c_int]),
         "kgs_pipeline_plan": (_I64, [_I64, _I64, _I64, ctypes.POINTER(_I64), _I64]),
+        "kgs_restore_backup": (ctypes.c_int, [_P]),
+        "kgs_step_program": (_I64, [_I64, ctypes.c_int, _I64, _I64, _I64, ctypes.c_int,
+                                    ctypes.POINTER(_I64), _I64]),
         "kgs_energy_terms": (ctypes.c_int, [_P, _DP]),
         "kgs_energy_mass": (ctypes.c_int, [_P, _D, _D, _D, _D, _DP, _DP]),
         "kgs_all_finite": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
@@ -100,6 +104,8 @@ def load() -> ctypes.CDLL:
         "kgs_last_step_ms": (_D, [_P]),
         "kgs_fill_preset": (ctypes.c_int, [_P, ctypes.c_int]),
         "kgs_abi_version": (ctypes.c_int, []),
+        "kgs_build_flags": (ctypes.c_int, []),
+        "kgs_device_count": (ctypes.c_int, []),
         "kgs_pass_timing": (ctypes.c_int, [_P, ctypes.c_int]),
         "kgs_pass_stats": (ctypes.c_int, [_P, ctypes.POINTER(_I64), _DP, ctypes.POINTER(_I64)]),
         "kgs_host_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(_P)]),
@@ -147,3 +153,32 @@ def coeffs_struct(kernel_args) -> KgsCoeffs:
     if len(vals) != 11:
         raise ValueError("expected the 11 kernel_args() scalars")
     return KgsCoeffs(*vals)
+
+
+# kgs_step_program row kinds (include/kgs_b200.h)
+PG_LAUNCH, PG_WAIT_XCH, PG_XCH, PG_RECORD, PG_DEFER, PG_PASS_BEGIN, PG_PASS_END = range(1, 8)
+KGS_PROGRAM_HEAD_FUSED = 2
+
+
+def step_program(nx: int, split: bool, nsteps: int, step_offset: int = 0,
+                 record_stride: int = 0, defer_tail: bool = False,
+                 head_fused: bool = False):
+    """The pass program kgs_step_dpavf2 runs on every slab / rank (pure host
+    logic in the C library; no device needed): an int64 array of rows
+    (kind, col, op1, op2, diag, check, step, xa, xb)."""
+    import numpy as np
+    lib = load()
+    flags = (KGS_STEP_DEFER_TAIL if defer_tail else 0) | (KGS_PROGRAM_HEAD_FUSED if head_fused
+                                                          else 0)
+    n = lib.kgs_step_program(nx, int(split), nsteps, step_offset, record_stride, flags, None, 0)
+    if n < 0:
+        raise ValueError("kgs_step_program: bad arguments")
+    out = np.zeros((max(n, 1), 9), dtype=np.int64)
+    lib.kgs_step_program(nx, int(split), nsteps, step_offset, record_stride, flags,
+                         out.ctypes.data_as(ctypes.POINTER(_I64)), n)
+    return out[:n]
+
+
+def device_count() -> int:
+    """CUDA devices the library sees (0 without a driver)."""
+    return max(0, int(load().kgs_device_count()))

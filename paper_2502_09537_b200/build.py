@@ -1,6 +1,6 @@
 """Build libkgs_b200.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_2502_09537_b200.build [--force]
+    python -m paper_2502_09537_b200.build [--force] [--checked] [--experimental]
 
 -fmad=false keeps the reference's un-contracted fp64 arithmetic
 (numba/LLVM without fastmath, dpavf/kernels.py:20) so results are bitwise
@@ -43,18 +43,24 @@ def up_to_date() -> bool:
 
 
 CHECKED_OUT = PKG / "libkgs_b200_checked.so"
+EXPERIMENTAL_OUT = PKG / "libkgs_b200_exp.so"
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, checked: bool = False,
+          experimental: bool = False) -> Path:
     """checked: -DKGS_CHECKED (index asserts that trap) into
-    libkgs_b200_checked.so, for tools/sanitize_run.py; never loaded by
-    default (select it with KGS_B200_LIB)."""
-    out = CHECKED_OUT if checked else OUT
-    if not force and not checked and up_to_date():
+    libkgs_b200_checked.so, for tools/sanitize_run.py; experimental:
+    -DKGS_EXPERIMENTAL (the slower fused one-march step, clustered /
+    producer-warp march variants, kgs_debug_pass) into
+    libkgs_b200_exp.so.  Neither is loaded by default (select one with
+    KGS_B200_LIB)."""
+    flags = (["-DKGS_CHECKED"] if checked else []) + (["-DKGS_EXPERIMENTAL"] if experimental
+                                                      else [])
+    out = (EXPERIMENTAL_OUT if experimental else CHECKED_OUT) if flags else OUT
+    if not force and not flags and up_to_date():
         return OUT
     tmp = out.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-DKGS_CHECKED"] if checked else []), "-o", str(tmp),
-           *map(str, SOURCES), "-ldl"]
+    cmd = [nvcc(), *NVCC_FLAGS, *flags, "-o", str(tmp), *map(str, SOURCES), "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
@@ -63,4 +69,5 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv,
+                experimental="--experimental" in sys.argv))

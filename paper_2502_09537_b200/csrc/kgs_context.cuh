@@ -4,7 +4,14 @@
 
 namespace {
 
-constexpr int kMarchVariantSlots = 7;   // march kernel variants (kgs_launch.cuh MV0..MV6)
+// march kernel variants (kgs_launch.cuh): MV0..MV3 tile shapes; the
+// clustered and producer-warp variants MV4..MV6 are experimental (slower,
+// DESIGN.md §5) and exist only in -DKGS_EXPERIMENTAL builds
+#ifdef KGS_EXPERIMENTAL
+constexpr int kMarchVariantSlots = 7;
+#else
+constexpr int kMarchVariantSlots = 4;
+#endif
 
 thread_local std::string g_last_error = "no error";
 
@@ -64,8 +71,10 @@ struct Slab {
   double* alt[2] = {nullptr, nullptr};
   double* alt0[2] = {nullptr, nullptr};
   MarchMaps amaps[kMarchVariantSlots][2];
+#ifdef KGS_EXPERIMENTAL
   StepMaps smap[2];        // red of [0] the current set, [1] the other set
   bool has_smap = false;
+#endif
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
   double* records = nullptr;                 // device [cap * NTERMS]
@@ -134,6 +143,7 @@ struct kgs_ctx {
   int64_t pass_no = 0;       // colour passes issued with the interior/boundary split
   bool mirrored[2] = {false, false};  // faces of colour c already in the ghosts
   bool alt_failed = false; // the second buffer set did not fit: two-pass steps
+  bool backup_valid = false;  // the second buffer set holds a KGS_STEP_BACKUP copy
   int64_t timed_pts = 0;   // points updated twice per timed launch
   // per-pass timing (slab 0's stream): event pairs around fused passes
   bool pass_timing = false;

@@ -25,14 +25,38 @@ using namespace kgs;
 
 #include "kgs_context.cuh"
 #include "kgs_launch.cuh"
+#include "kgs_program.cuh"
 #include "kgs_passes.cuh"
+#ifdef KGS_EXPERIMENTAL
+#include "kgs_exp_step.cuh"
+#endif
 
 // =========================================================================
 // extern "C" API
 // =========================================================================
 extern "C" {
 
-int kgs_abi_version(void) { return 100; }
+int kgs_abi_version(void) { return 101; }
+
+int kgs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int kgs_build_flags(void) {
+  int f = 0;
+#ifdef KGS_EXPERIMENTAL
+  f |= KGS_BUILD_EXPERIMENTAL;
+#endif
+#ifdef KGS_CHECKED
+  f |= KGS_BUILD_CHECKED;
+#endif
+  return f;
+}
 
 const char* kgs_last_error(kgs_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_last_error.c_str();
@@ -256,6 +280,7 @@ extern "C" {
 int kgs_upload(kgs_ctx* ctx, const double* P, const double* Q, const double* U,
                const double* V) {
   if (!ctx || !P || !Q || !U || !V) return fail(ctx, KGS_EINVAL, "NULL argument");
+  ctx->backup_valid = false;
   ctx->pending = false;  // the whole state is replaced
   const double* f[4] = {P, Q, U, V};
   int64_t x0, nx;
@@ -288,6 +313,7 @@ int kgs_upload_planes(kgs_ctx* ctx, int field, int64_t x_begin, int64_t nplanes,
                       const double* src) {
   int r = check_range(ctx, field, x_begin, nplanes, src);
   if (r) return r;
+  ctx->backup_valid = false;
   r = flush_pending(ctx);
   if (!r) r = transfer_planes(ctx, field, x_begin, nplanes, const_cast<double*>(src), true);
   ctx->mirrored[0] = ctx->mirrored[1] = false;  // planes written without mirroring
@@ -310,6 +336,7 @@ int kgs_sweep(kgs_ctx* ctx, int colour, int kind, const kgs_coeffs* c) {
   if (colour != 0 && colour != 1) return fail(ctx, KGS_EINVAL, "colour must be 0 or 1");
   if (kind != 0 && kind != 1) return fail(ctx, KGS_EINVAL, "kind must be 0 (base) or 1 (adjoint)");
   const Coeffs k = to_coeffs(c);
+  ctx->backup_valid = false;
   int r = flush_pending(ctx);
   if (!r) r = all_passes(ctx, colour, kind == 0 ? OP_BASE : OP_ADJ, OP_NONE, false, false, k, 0);
   if (!r) r = exchange(ctx, colour);
@@ -333,6 +360,22 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
   int r = ensure_records(ctx, nrec);
   if (!r) r = reset_bad(ctx);
   if (r) return r;
+  ctx->backup_valid = false;
+  if (flags & KGS_STEP_BACKUP) {
+    // the state at step_offset (a pending tail applied first) into the
+    // second buffer set, ghosts included, for kgs_restore_backup
+    r = flush_pending(ctx);
+    if (!r && ensure_alt(ctx) == KGS_OK) {
+      for (auto& s : ctx->slabs) {
+        CK(cudaSetDevice(s.dev));
+        for (int cc = 0; cc < 2; ++cc)
+          CK(cudaMemcpyAsync(s.alt[cc], s.buf[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
+                             cudaMemcpyDeviceToDevice, s.stream));
+      }
+      ctx->backup_valid = true;
+    }
+    if (r) return r;
+  }
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
     CK(cudaEventRecord(s.ev_t0, s.stream));
@@ -342,51 +385,38 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
                      !(record_stride > 0 && last % record_stride == 0);
   const bool resident = resident_eligible(ctx);
   // head: base red(first step) -- fused with a deferred red adjoint of the
-  // previous call when its coefficients are the same (bitwise neutral)
+  // previous call when its coefficients are the same (bitwise neutral);
+  // a pending adjoint with other coefficients is applied first
   const bool head_fused = ctx->pending && std::memcmp(&ctx->pend_c, &c, sizeof c) == 0;
-  if (head_fused) {
-    ctx->pending = false;
-    if (!resident) r = all_passes(ctx, 1, OP_ADJ, OP_BASE, false, false, c, 0);
-  } else {
-    r = flush_pending(ctx);
-    if (!r && !resident) r = all_passes(ctx, 1, OP_BASE, OP_NONE, false, false, c, 0);
-  }
-  if (!r && resident) {
+  if (head_fused) ctx->pending = false;
+  else r = flush_pending(ctx);
+#ifdef KGS_EXPERIMENTAL
+  const bool fused = !resident && fused_ready(ctx);
+#else
+  constexpr bool fused = false;
+#endif
+  if (r) {
+  } else if (resident) {
     // the whole call in one launch (state in shared memory)
     r = launch_resident(ctx, c, nsteps, step_offset, record_stride, head_fused, defer);
     if (!r && defer) {
       ctx->pending = true;
       ctx->pend_c = c;
     }
-    nsteps = 0;   // skip the per-step loop below
+  } else if (!fused) {
+    // the pass program (kgs_program.cuh): head, K3/K4 per step, exchanges,
+    // records, deferred tail -- the same list kgs_step_program exports
+    const Program prog = step_program(ctx->slabs[0].nx, needs_exchange(ctx), nsteps,
+                                      step_offset, record_stride,
+                                      (head_fused ? PGF_HEAD_FUSED : 0) |
+                                          ((flags & KGS_STEP_DEFER_TAIL) ? PGF_DEFER : 0));
+    r = run_program(ctx, prog, c);
   }
-  if (!r && !resident) r = exchange(ctx, 1);
-  int64_t slot = 0;
-  const bool fused = fused_ready(ctx);
-  int64_t all_pts = 0;
-  for (auto& s : ctx->slabs) all_pts += (int64_t)s.nx * ctx->ny * ctx->nk * 2;
-  for (int64_t i = 1; i <= nsteps && !r; ++i) {
-    const int64_t n = step_offset + i;
-    const bool rec = record_stride > 0 && n % record_stride == 0;
-    if (fused && !(i == nsteps && defer)) {
-      // one fused march: K3(n) and K4(n) (the tail adjoint on the last step)
-      r = timed(ctx, all_pts, [&] { return step_fused(ctx, rec, i == nsteps, c, (int)n); });
-      if (!r && rec) r = finalize_record(ctx, slot++, false);
-      continue;
-    }
-    // K3: black base(n) + adjoint(n)
-    r = timed_passes(ctx, 0, OP_BASE, OP_ADJ, rec, true, c, (int)n);
-    if (!r) r = exchange(ctx, 0);
-    // K4: red adjoint(n) + base(n+1), or the tail: red adjoint(last)
-    if (!r && i < nsteps) r = timed_passes(ctx, 1, OP_ADJ, OP_BASE, rec, true, c, (int)n);
-    else if (!r && defer) {  // leave the red adjoint of the last step pending
-      ctx->pending = true;
-      ctx->pend_c = c;
-      break;
-    } else if (!r) r = all_passes(ctx, 1, OP_ADJ, OP_NONE, rec, true, c, (int)n);
-    if (!r) r = exchange(ctx, 1);
-    if (!r && rec) r = finalize_record(ctx, slot++, true);
+#ifdef KGS_EXPERIMENTAL
+  else {
+    r = step_loop_fused(ctx, c, nsteps, step_offset, record_stride, head_fused, defer);
   }
+#endif
   if (r) return r;
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
@@ -424,6 +454,25 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
   return KGS_OK;
 }
 
+int kgs_restore_backup(kgs_ctx* ctx) {
+  if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  if (!ctx->backup_valid)
+    return fail(ctx, KGS_EINVAL, "no backup: the last kgs_step_dpavf2 call had no "
+                "KGS_STEP_BACKUP (or no memory for it), or the state changed since");
+  for (auto& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.cstream));
+    for (int cc = 0; cc < 2; ++cc)
+      CK(cudaMemcpyAsync(s.buf[cc], s.alt[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
+                         cudaMemcpyDeviceToDevice, s.stream));
+    s.xch_pending = false;
+  }
+  ctx->pending = false;                          // the backup is a complete state
+  ctx->mirrored[0] = ctx->mirrored[1] = false;   // ghosts restored with it
+  ctx->backup_valid = false;
+  return sync_all(ctx);
+}
+
 int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
   if (!ctx || !terms_out) return fail(ctx, KGS_EINVAL, "NULL argument");
   Coeffs dummy{};
@@ -443,6 +492,24 @@ int kgs_energy_terms(kgs_ctx* ctx, double* terms_out) {
     for (int q = 0; q < NTERMS; ++q) terms_out[q] += tmp[q];
   }
   return KGS_OK;
+}
+
+int64_t kgs_step_program(int64_t nx, int split, int64_t nsteps, int64_t step_offset,
+                         int64_t record_stride, int flags, int64_t* out, int64_t cap) {
+  if (nx < 1 || (split && nx < 2) || nsteps < 0 || step_offset < 0 || record_stride < 0 ||
+      nsteps + step_offset > INT_MAX || cap < 0 || (cap > 0 && !out))
+    return -1;
+  const Program p = step_program(nx, split != 0, nsteps, step_offset, record_stride,
+                                 ((flags & KGS_PROGRAM_HEAD_FUSED) ? PGF_HEAD_FUSED : 0) |
+                                     ((flags & KGS_STEP_DEFER_TAIL) ? PGF_DEFER : 0));
+  const int64_t n = (int64_t)p.size();
+  for (int64_t i = 0; i < std::min(n, cap); ++i) {
+    const ProgOp& o = p[i];
+    const int64_t row[kProgFields] = {o.kind, o.col, o.op1, o.op2, o.diag, o.check, o.step,
+                                      o.xa, o.xb};
+    std::copy(row, row + kProgFields, out + kProgFields * i);
+  }
+  return n;
 }
 
 int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap) {
@@ -465,6 +532,7 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
   (void)flags;
   if (!ctx || !P || !Q || !U || !V || !half || !terms0)
     return fail(ctx, KGS_EINVAL, "NULL argument");
+  ctx->backup_valid = false;   // the pipeline uses the second buffer set itself
   if (nsteps < 0 || record_stride < 0 || step_offset < 0)
     return fail(ctx, KGS_EINVAL, "negative nsteps/step_offset/record_stride");
   if (nsteps + step_offset > INT_MAX) return fail(ctx, KGS_EINVAL, "step numbers too large");
@@ -587,6 +655,11 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
 
 int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   if (!ctx || !ms_out || reps < 1) return fail(ctx, KGS_EINVAL, "bad arguments");
+#ifndef KGS_EXPERIMENTAL
+  (void)mode;
+  return fail(ctx, KGS_EINVAL, "kgs_debug_pass needs a -DKGS_EXPERIMENTAL build "
+              "(python -m paper_2502_09537_b200.build --experimental)");
+#else
   Slab& s = ctx->slabs[0];
   PassGeom g = make_geom(ctx, s, 0, 0, s.nx);
   const int v = march_variant(ctx, s, g);
@@ -624,6 +697,7 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   if (e != cudaSuccess) return fail(ctx, KGS_ECUDA, "debug pass: %s", cudaGetErrorString(e));
   *ms_out = ms / reps;
   return KGS_OK;
+#endif
 }
 
 int kgs_selftest_division(int device, int64_t n, uint64_t seed, int64_t* mismatches) {
@@ -661,10 +735,20 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   if (!ctx || !name) return fail(ctx, KGS_EINVAL, "NULL argument");
   const std::string n(name);
   if (n == "march_sync") ctx->tune_sync = std::max(1, value);
-  else if (n == "march_variant") ctx->tune_variant = value;
+  else if (n == "march_variant") {
+    if (value >= kMarchVariantSlots)
+      return fail(ctx, KGS_EINVAL, "march_variant %d not in this build (0..%d; 4..6 need "
+                  "-DKGS_EXPERIMENTAL)", value, kMarchVariantSlots - 1);
+    ctx->tune_variant = value;
+  }
   else if (n == "march_planes") ctx->tune_xc = value;
   else if (n == "blocks_per_sm") ctx->tune_occ = value;
-  else if (n == "fused_step") ctx->tune_fused = value;
+  else if (n == "fused_step") {
+#ifndef KGS_EXPERIMENTAL
+    if (value) return fail(ctx, KGS_EINVAL, "fused_step needs a -DKGS_EXPERIMENTAL build");
+#endif
+    ctx->tune_fused = value;
+  }
   else if (n == "fused_planes") ctx->tune_fused_xc = std::max(1, value);
   else if (n == "fused_debug") ctx->tune_fused_dbg = value;
   else if (n == "resident") ctx->tune_resident = value;
@@ -697,6 +781,7 @@ int kgs_pass_stats(kgs_ctx* ctx, int64_t* launches, double* total_ms,
 
 int kgs_fill_preset(kgs_ctx* ctx, int preset) {
   if (!ctx) return fail(nullptr, KGS_EINVAL, "ctx is NULL");
+  ctx->backup_valid = false;
   ctx->pending = false;  // the whole state is replaced
   const int need_d[4] = {3, 2, 2, 1};
   if (preset < 0 || preset > 3) return fail(ctx, KGS_EINVAL, "unknown preset %d", preset);

@@ -82,6 +82,8 @@ int exchange(kgs_ctx* ctx, int col) {
   return KGS_OK;
 }
 
+int finalize_record(kgs_ctx* ctx, int64_t slot, bool both);
+
 int sync_all(kgs_ctx* ctx) {
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
@@ -91,67 +93,144 @@ int sync_all(kgs_ctx* ctx) {
   return KGS_OK;
 }
 
-// One colour pass over every slab.  With several slabs (or ranks) the
-// interior planes [1, nx-1) go first -- they need no ghost data, so they
-// overlap the previous pass's halo exchange -- then the stream waits for
-// that exchange (ev_xch) and runs the two boundary planes.
-//
-// Fused halo exchange (ctx->mirror): the boundary launches of slab i also
-// store their new faces into the neighbours' ghost planes (peer pointers),
-// so no exchange follows.  Before slab i's boundary launches of pass k its
-// stream waits for both neighbours' boundary launches of pass k-1 (ev_face):
-// that is when they finished writing i's ghosts (RAW) and finished reading
-// their own ghosts that i is about to overwrite (WAR); pending copy
-// exchanges into either side are waited for as well.
-int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
-               const Coeffs& c, int step_no) {
+// ---- program executor (kgs_program.cuh) --------------------------------
+// Every slab executes the program in order on its compute stream; halo
+// exchanges run on its comm stream.  Ordering is by stream events only:
+//  * PG_XCH records ev_bnd (the faces are written) and starts the exchange
+//    (NCCL send/recv or peer copies) on the comm stream, completing ev_xch;
+//  * PG_WAIT_XCH makes the compute stream wait for ev_xch -- placed after
+//    a pass's interior launch, so the interior overlaps the transfer, and
+//    before the boundary launches that read the ghosts.
+// Fused halo exchange (ctx->mirror: single process, peer-accessible
+// neighbours): the boundary launches of slab i also store their new faces
+// into the neighbours' ghost planes (peer pointers), so the PG_XCH that
+// follows is a no-op.  Then PG_WAIT_XCH of pass k also waits for both
+// neighbours' boundary launches of pass k-1 (ev_face): that is when they
+// finished writing i's ghosts (RAW) and finished reading their own ghosts
+// that i is about to overwrite (WAR); pending copy exchanges into either
+// side (after uploads) are waited for as well.
+int run_program(kgs_ctx* ctx, const Program& prog, const Coeffs& c) {
   const bool split = needs_exchange(ctx);
   const bool mirror = split && ctx->mirror && ctx->tune_mirror;
-  const bool writes = op1 != OP_NONE || op2 != OP_NONE;
-  const int64_t k = ctx->pass_no;
-  if (split) ctx->pass_no++;
   const int ns = (int)ctx->slabs.size();
-  for (int i = 0; i < ns; ++i) {
-    Slab& s = ctx->slabs[i];
-    cudaError_t e = cudaSetDevice(s.dev);
-    if (e != cudaSuccess) return fail(ctx, KGS_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
-    if (diag) s.npart[col] = 0;
-    int r;
-    if (!split) {
-      r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no);
-    } else {
-      r = KGS_OK;
-      if (s.nx > 2) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, 1, s.nx - 1);
-      if (!r && s.xch_pending) {
-        CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
-        s.xch_pending = false;
-      }
-      Slab& lo = ctx->slabs[(i - 1 + ns) % ns];
-      Slab& hi = ctx->slabs[(i + 1) % ns];
-      if (!r && mirror) {
-        CK(cudaStreamWaitEvent(s.stream, lo.ev_xch, 0));
-        CK(cudaStreamWaitEvent(s.stream, hi.ev_xch, 0));
-        if (k > 0) {
-          CK(cudaStreamWaitEvent(s.stream, lo.ev_face[(k - 1) & 1], 0));
-          CK(cudaStreamWaitEvent(s.stream, hi.ev_face[(k - 1) & 1], 0));
+  int64_t k = 0;            // number of the current pass (fused halo stores)
+  bool in_pass = false, writes = false, timing = false;
+  int pcol = 0;
+  for (const ProgOp& o : prog) {
+    switch (o.kind) {
+      case PG_PASS_BEGIN: {
+        in_pass = true;
+        pcol = o.col;
+        writes = o.op1 != OP_NONE || o.op2 != OP_NONE;
+        k = ctx->pass_no;
+        if (split) ctx->pass_no++;
+        int64_t pts = 0;
+        for (auto& s : ctx->slabs) {
+          if (o.diag) s.npart[o.col] = 0;
+          pts += (int64_t)s.nx * ctx->ny * ctx->nk;
         }
+        timing = o.xa && ctx->pass_timing;
+        if (o.xa) ctx->timed_pts = pts;
+        if (timing) {   // event pair on slab 0's stream around the fused pass
+          Slab& s0 = ctx->slabs[0];
+          CK(cudaSetDevice(s0.dev));
+          if (ctx->pass_ev_used + 2 > ctx->pass_ev.size())
+            for (int i = 0; i < 64; ++i) {
+              cudaEvent_t e;
+              CK(cudaEventCreate(&e));
+              ctx->pass_ev.push_back(e);
+            }
+          CK(cudaEventRecord(ctx->pass_ev[ctx->pass_ev_used++], s0.stream));
+        }
+        break;
       }
-      // our plane 0 is lo's ghost plane lo.nx; our plane nx-1 is hi's ghost -1
-      double* mlo = (mirror && writes) ? lo.plane0[col] + (int64_t)lo.nx * ctx->ps : nullptr;
-      double* mhi = (mirror && writes) ? hi.plane0[col] - ctx->ps : nullptr;
-      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, 0, 1, nullptr,
-                              mlo, nullptr);
-      if (!r) r = launch_pass(ctx, s, col, op1, op2, diag, check, c, step_no, s.nx - 1, s.nx,
-                              nullptr, nullptr, mhi);
-      if (!r && mirror) CK(cudaEventRecord(s.ev_face[k & 1], s.stream));
+      case PG_LAUNCH:
+        for (int i = 0; i < ns; ++i) {
+          Slab& s = ctx->slabs[i];
+          cudaError_t e = cudaSetDevice(s.dev);
+          if (e != cudaSuccess)
+            return fail(ctx, KGS_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+          const int xb = std::min(o.xb, s.nx);
+          // our plane 0 is lo's ghost plane lo.nx; our plane nx-1 is hi's ghost -1
+          double* mlo = nullptr;
+          double* mhi = nullptr;
+          if (mirror && writes) {
+            Slab& lo = ctx->slabs[(i - 1 + ns) % ns];
+            Slab& hi = ctx->slabs[(i + 1) % ns];
+            if (o.xa == 0) mlo = lo.plane0[o.col] + (int64_t)lo.nx * ctx->ps;
+            if (xb == s.nx) mhi = hi.plane0[o.col] - ctx->ps;
+          }
+          int r = launch_pass(ctx, s, o.col, o.op1, o.op2, o.diag != 0, o.check != 0, c, o.step,
+                              o.xa, xb, nullptr, mlo, mhi);
+          if (r) return r;
+        }
+        break;
+      case PG_WAIT_XCH:
+        for (int i = 0; i < ns; ++i) {
+          Slab& s = ctx->slabs[i];
+          CK(cudaSetDevice(s.dev));
+          if (s.xch_pending) {
+            CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+            s.xch_pending = false;
+          }
+          if (mirror && in_pass) {
+            Slab& lo = ctx->slabs[(i - 1 + ns) % ns];
+            Slab& hi = ctx->slabs[(i + 1) % ns];
+            CK(cudaStreamWaitEvent(s.stream, lo.ev_xch, 0));
+            CK(cudaStreamWaitEvent(s.stream, hi.ev_xch, 0));
+            if (k > 0) {
+              CK(cudaStreamWaitEvent(s.stream, lo.ev_face[(k - 1) & 1], 0));
+              CK(cudaStreamWaitEvent(s.stream, hi.ev_face[(k - 1) & 1], 0));
+            }
+          }
+        }
+        break;
+      case PG_PASS_END:
+        if (mirror)
+          for (auto& s : ctx->slabs) {
+            CK(cudaSetDevice(s.dev));
+            CK(cudaEventRecord(s.ev_face[k & 1], s.stream));
+          }
+        if (mirror && writes) ctx->mirrored[pcol] = true;
+        if (timing) {
+          Slab& s0 = ctx->slabs[0];
+          CK(cudaSetDevice(s0.dev));
+          CK(cudaEventRecord(ctx->pass_ev[ctx->pass_ev_used++], s0.stream));
+        }
+        in_pass = timing = false;
+        break;
+      case PG_XCH: {
+        int r = exchange(ctx, o.col);
+        if (r) return r;
+        break;
+      }
+      case PG_RECORD: {
+        int r = finalize_record(ctx, o.step, o.xa != 0);
+        if (r) return r;
+        break;
+      }
+      case PG_DEFER:
+        ctx->pending = true;
+        ctx->pend_c = c;
+        break;
+      default:
+        return fail(ctx, KGS_EINVAL, "bad program op %d", o.kind);
     }
-    if (r) return r;
   }
-  if (mirror && writes) ctx->mirrored[col] = true;
   return KGS_OK;
 }
 
-// Run `launch` bracketed by an event pair on slab 0's stream when timing.
+// One colour pass over every slab (no exchange after it).
+int all_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
+               const Coeffs& c, int step_no) {
+  const Program p = pass_program(ctx->slabs[0].nx, needs_exchange(ctx), col, op1, op2, diag,
+                                 check, step_no, false);
+  return run_program(ctx, p, c);
+}
+
+#ifdef KGS_EXPERIMENTAL
+// Run `launch` bracketed by an event pair on slab 0's stream when timing
+// (the experimental fused step).
 template <class F>
 int timed(kgs_ctx* ctx, int64_t pts, F&& launch) {
   ctx->timed_pts = pts;
@@ -175,33 +254,7 @@ int timed(kgs_ctx* ctx, int64_t pts, F&& launch) {
   CK(cudaEventRecord(b, s0.stream));
   return KGS_OK;
 }
-
-// all_passes() bracketed by an event pair on slab 0's stream when timing.
-int timed_passes(kgs_ctx* ctx, int col, int op1, int op2, bool diag, bool check,
-                 const Coeffs& c, int step_no) {
-  int64_t pts = 0;
-  for (auto& s : ctx->slabs) pts += (int64_t)s.nx * ctx->ny * ctx->nk;
-  ctx->timed_pts = pts;
-  if (!ctx->pass_timing) return all_passes(ctx, col, op1, op2, diag, check, c, step_no);
-  Slab& s0 = ctx->slabs[0];
-  if (ctx->pass_ev_used + 2 > ctx->pass_ev.size()) {
-    CK(cudaSetDevice(s0.dev));
-    for (int i = 0; i < 64; ++i) {
-      cudaEvent_t e;
-      CK(cudaEventCreate(&e));
-      ctx->pass_ev.push_back(e);
-    }
-  }
-  cudaEvent_t a = ctx->pass_ev[ctx->pass_ev_used++];
-  cudaEvent_t b = ctx->pass_ev[ctx->pass_ev_used++];
-  CK(cudaSetDevice(s0.dev));
-  CK(cudaEventRecord(a, s0.stream));
-  int r = all_passes(ctx, col, op1, op2, diag, check, c, step_no);
-  if (r) return r;
-  CK(cudaSetDevice(s0.dev));
-  CK(cudaEventRecord(b, s0.stream));
-  return KGS_OK;
-}
+#endif
 
 int collect_pass_times(kgs_ctx* ctx) {
   for (size_t i = 0; i + 1 < ctx->pass_ev_used; i += 2) {

@@ -194,9 +194,11 @@ class DeviceContext:
         return terms0, terms[:nrec], (bad.value if rc == _lib.KGS_ENONFINITE else 0)
 
     def step_dpavf2(self, kernel_args, nsteps: int, step_offset: int = 0,
-                    record_stride: int = 0, defer_tail: bool = False):
+                    record_stride: int = 0, defer_tail: bool = False, backup: bool = False):
         """Run nsteps fused DP-AVF2 steps; returns (terms[nrec, 8], bad_step).
-        defer_tail: leave the last red adjoint pending (see kgs_b200.h)."""
+        defer_tail: leave the last red adjoint pending (see kgs_b200.h);
+        backup: keep a device copy of the starting state for
+        restore_backup()."""
         lib = _lib.load()
         c = _lib.coeffs_struct(kernel_args)
         if record_stride > 0:
@@ -207,7 +209,8 @@ class DeviceContext:
         bad = ctypes.c_int64(0)
         rc = lib.kgs_step_dpavf2(self.ptr, ctypes.byref(c), nsteps, step_offset,
                                  record_stride, _lib.dptr(terms), ctypes.byref(bad),
-                                 _lib.KGS_STEP_DEFER_TAIL if defer_tail else 0)
+                                 (_lib.KGS_STEP_DEFER_TAIL if defer_tail else 0)
+                                 | (_lib.KGS_STEP_BACKUP if backup else 0))
         if rc not in (_lib.KGS_OK, _lib.KGS_ENONFINITE):
             self.check(rc)
         bad_step = bad.value if rc == _lib.KGS_ENONFINITE else 0
@@ -218,6 +221,11 @@ class DeviceContext:
             bads = [b for _, b in gathered if b]
             bad_step = min(bads) if bads else 0
         return terms, bad_step
+
+    def restore_backup(self) -> bool:
+        """Back to the state saved by the last step_dpavf2(..., backup=True);
+        False if there is none (no memory for it, or the state changed)."""
+        return _lib.load().kgs_restore_backup(self.ptr) == _lib.KGS_OK
 
     def fill_preset(self, name: str) -> None:
         if name not in PRESETS:

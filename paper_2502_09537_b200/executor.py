@@ -50,16 +50,17 @@ class ExecutorConfig:
             return PhasedExecutor(self.workers)
         # one slab per GPU; with fewer GPUs than workers, virtual slabs on
         # cuda:0 (same results bitwise: decomposition invariance)
-        n = _device_count()
-        if self.workers <= max(n, 1) or n == 0:
+        if self.workers <= _device_count():
             return CudaExecutor(tuple(range(self.workers)))
         return CudaExecutor((0,), slabs_per_device=self.workers)
 
 
 def _device_count() -> int:
+    """CUDA devices visible to the library (kgs_device_count, i.e.
+    cudaGetDeviceCount); 0 without a driver or library."""
     try:
-        import torch
-        return torch.cuda.device_count()
+        from . import _lib
+        return _lib.device_count()
     except Exception:
         return 0
 

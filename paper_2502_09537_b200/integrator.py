@@ -26,7 +26,7 @@ import numpy as np
 
 from .device import DeviceFieldState, as_device_state, get_context
 from .grid import FieldState, GridSpec, PhysParams, energy_from_terms
-from .ordering import BLACK, RED, UpdateSchedule, require_checkerboard
+from .ordering import colour_order, is_reversed, require_checkerboard
 
 KIND_BASE, KIND_ADJOINT = 0, 1
 
@@ -71,8 +71,11 @@ def precompute_coefficients(params: PhysParams, tau: float,
                             tau * params.kappa2 / h2, tau * params.gamma, uv_inv)
 
 
-def _colours(schedule, adjoint: bool) -> tuple[int, int]:
-    order = schedule.colour_order if isinstance(schedule, UpdateSchedule) else (RED, BLACK)
+def _colours(schedule, grid: GridSpec, adjoint: bool) -> tuple[int, int]:
+    """Colour order of one sweep: the schedule's own (ours, or the
+    reference's UpdateSchedule incl. reverse_schedule'd ones), reversed for
+    the adjoint (integrator.py:115-121)."""
+    order = colour_order(schedule, grid)
     return tuple(reversed(order)) if adjoint else order
 
 
@@ -81,7 +84,7 @@ def _sweep(state, schedule, coeffs: StepCoefficients, executor, grid: GridSpec,
     require_checkerboard(schedule, grid)
     dev, temp = as_device_state(state, grid, executor)
     args = coeffs.kernel_args()
-    for colour in _colours(schedule, kind == KIND_ADJOINT):
+    for colour in _colours(schedule, grid, kind == KIND_ADJOINT):
         dev.ctx.sweep(colour, kind, args)
     if temp:
         dev.ctx.download(state)
@@ -107,7 +110,7 @@ def step_dpavf2(state, schedule, coeffs_half: StepCoefficients, executor,
     """Symmetric composition: base then adjoint, each at tau/2
     (reference integrator.py:124-129), as one fused device call."""
     require_checkerboard(schedule, grid)
-    if isinstance(schedule, UpdateSchedule) and schedule.reversed:
+    if is_reversed(schedule, grid):
         # a reversed schedule swaps the colour order of both halves
         step_base(state, schedule, coeffs_half, executor, grid)
         step_adjoint(state, schedule, coeffs_half, executor, grid)
@@ -167,6 +170,40 @@ def _append_records(trace, terms, k0, k1, record_stride, t, e0, absolute, params
     return t
 
 
+def _integrate_stepwise(state, grid, params, schedule, executor, tau, n_steps, record_stride,
+                        snapshot_stride, snapshot_writer) -> EnergyTrace:
+    """The reference loop (integrator.py:159-182) one step_dpavf2 call at a
+    time -- for schedules the fused loop does not cover (a reversed
+    checkerboard: black sweeps first in both halves)."""
+    coeffs_half = precompute_coefficients(params, tau / 2.0, grid)
+    dev, temp = as_device_state(state, grid, executor)
+    e0, m0 = energy_from_terms(dev.energy_terms(), params, grid)
+    absolute = abs(e0) < 1e-300
+    trace = EnergyTrace([0], [state.t], [e0], [0.0], [m0], re_is_absolute=absolute)
+    for n in range(1, n_steps + 1):
+        step_dpavf2(dev, schedule, coeffs_half, executor, grid)
+        state.t = dev.t
+        if not dev.is_finite():
+            if temp:
+                dev.ctx.download(state)
+            raise FloatingPointError(
+                f"non-finite field values detected after step {n} (t={state.t})")
+        if n % record_stride == 0:
+            e, m = energy_from_terms(dev.energy_terms(), params, grid)
+            trace.steps.append(n)
+            trace.times.append(state.t)
+            trace.energy.append(e)
+            trace.rel_error.append(abs(e - e0) if absolute else abs(e - e0) / abs(e0))
+            trace.mass.append(m)
+        if snapshot_stride and snapshot_writer and n % snapshot_stride == 0:
+            if temp:
+                dev.ctx.download(state)
+            snapshot_writer(state, n)
+    if temp:
+        dev.ctx.download(state)
+    return trace
+
+
 def integrate(state, grid: GridSpec, params: PhysParams,
               schedule, executor, tau: float, T: float,
               record_stride: int = 1, snapshot_stride: int = 0,
@@ -184,9 +221,10 @@ def integrate(state, grid: GridSpec, params: PhysParams,
     if record_stride < 1:
         raise ValueError("record_stride must be >= 1")
     require_checkerboard(schedule, grid)
-    if isinstance(schedule, UpdateSchedule) and schedule.reversed:
-        raise ValueError("integrate expects the forward checkerboard schedule")
     n_steps = int(math.ceil(T / tau - 1e-12)) if T > 0 else 0
+    if is_reversed(schedule, grid):
+        return _integrate_stepwise(state, grid, params, schedule, executor, tau, n_steps,
+                                   record_stride, snapshot_stride, snapshot_writer)
     coeffs_half = precompute_coefficients(params, tau / 2.0, grid)
     args = coeffs_half.kernel_args()
 
@@ -227,14 +265,26 @@ def integrate(state, grid: GridSpec, params: PhysParams,
     while n < n_steps:
         n1 = n_steps if not snap else min(n_steps, (n // snap + 1) * snap)
         t_start = state.t
-        terms, bad = dev.ctx.step_dpavf2(args, n1 - n, n, record_stride)
+        # a device-resident state keeps a device copy of the chunk start so
+        # a non-finite step can be replayed exactly (host states are re-uploaded)
+        terms, bad = dev.ctx.step_dpavf2(args, n1 - n, n, record_stride,
+                                         backup=host is None)
         if bad:
             if host is not None:
                 # restore the step-n host state and replay exactly to `bad`
                 dev.ctx.upload(host)
                 dev.ctx.step_dpavf2(args, bad - n, n, 0)
                 dev.ctx.download(host)
-            state.t = advance_t(t_start, bad - n)
+                state.t = advance_t(t_start, bad - n)
+            elif dev.ctx.restore_backup():
+                dev.ctx.step_dpavf2(args, bad - n, n, 0)
+                state.t = advance_t(t_start, bad - n)
+            else:   # no memory for the copy: fields and t both after step n1
+                state.t = advance_t(t_start, n1 - n)
+                raise FloatingPointError(
+                    f"non-finite field values detected after step {bad} (t="
+                    f"{advance_t(t_start, bad - n)}); the device state could not be "
+                    f"rewound and is left after step {n1} (t={state.t})")
             raise FloatingPointError(
                 f"non-finite field values detected after step {bad} (t={state.t})")
         state.t = _append_records(trace, terms, n + 1, n1, record_stride, t_start, e0,

@@ -128,6 +128,36 @@ def validate_schedule(s, grid: GridSpec) -> str | None:
     return None
 
 
+def colour_order(s, grid: GridSpec) -> tuple[int, int]:
+    """The colours of a checkerboard schedule in sweep order.  Ours carry it
+    (``reversed``); for the reference's UpdateSchedule objects it is read off
+    the schedule itself -- the colour of the first point of its first phase
+    (ordering.py:130-146: red first, or black first after
+    ``reverse_schedule``), else of the point with rank 0."""
+    if isinstance(s, UpdateSchedule):
+        return s.colour_order
+    first = None
+    phases = getattr(s, "phases", None)
+    if phases:
+        for lane in phases[0].lanes:
+            if len(lane):
+                first = int(lane[0])
+                break
+    if first is None:
+        rank = getattr(s, "rank", None)
+        if rank is not None and len(rank):
+            first = int(np.argmin(rank))
+    if first is None:
+        return (RED, BLACK)
+    parity = int(sum(np.unravel_index(first, grid.shape))) % 2
+    return (RED, BLACK) if parity == RED else (BLACK, RED)
+
+
+def is_reversed(s, grid: GridSpec) -> bool:
+    """True for a schedule that sweeps black before red (reverse_schedule)."""
+    return colour_order(s, grid)[0] == BLACK
+
+
 def require_checkerboard(s, grid: GridSpec) -> None:
     report = validate_schedule(s, grid)
     if report is not None:

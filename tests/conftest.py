@@ -19,6 +19,22 @@ from paper_2502_09537_b200 import FieldState, GridSpec, PhysParams  # noqa: E402
 GOLDEN = ROOT / "tests" / "golden" / "kgs_golden.npz"
 
 
+def experimental_build() -> bool:
+    """The loaded library was built with -DKGS_EXPERIMENTAL (build.py
+    --experimental, selected with KGS_B200_LIB): the slower fused one-march
+    step, march variants 4..6 and kgs_debug_pass are only there."""
+    try:
+        from paper_2502_09537_b200 import _lib
+        return bool(_lib.load().kgs_build_flags() & 1)
+    except Exception:
+        return False
+
+
+needs_experimental = pytest.mark.skipif(
+    not experimental_build(), reason="experimental kernels: needs libkgs_b200_exp.so "
+                                     "(KGS_B200_LIB, build.py --experimental)")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu)")
 

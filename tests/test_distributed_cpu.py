@@ -1,18 +1,27 @@
-"""CPU, multi-process (gloo): the N>1 host logic of the slab decomposition.
+"""CPU, multi-process (gloo): the N>1 schedule of the C++ library replayed.
 
-The device path splits the grid into slabs along axis 0; before every colour
-pass each rank receives the other colour's freshly updated face planes from
-ranks rank-1 / rank+1 (periodic) -- NCCL send/recv in
-paper_2502_09537_b200/csrc/kgs_host.cu:exchange(), with the send/recv order
-rule that keeps 2-rank rings (where both neighbours are the same peer)
-matched.  Energy terms are summed in rank order after an all-gather.
+A multi-GPU run (torchrun, one rank per GPU) splits the grid into slabs along
+axis 0.  What every rank does, in order, is the pass program of
+kgs_step_dpavf2 (csrc/kgs_program.cuh): colour-pass launches over plane
+ranges (interior first, boundary planes after the halo wait), halo
+exchanges of one colour's faces (P, Q, U of planes 0 and nx-1 into the
+neighbours' ghost planes -- NCCL send/recv on the device), waits for them,
+energy records and the deferred tail.  The library exports that exact list
+(``kgs_step_program``, the same function the device executor runs), so
+these tests fetch it from the C library and EXECUTE it in gloo worlds of 2
+and 4 ranks: launches with the numpy restatement of the per-point
+arithmetic (oracle/), exchanges with real send/recv of only that colour's
+face values (the other colour's ghosts stay stale, V ghosts are NaN), energy
+partials reduced at the records and summed in rank order.
 
-These tests run that protocol with gloo processes on the CPU: each rank
-steps its slab with the numpy colour-phase restatement (oracle/), exchanges
-faces with the same order rule through torch.distributed, and the result
-must be bitwise equal to the single-process oracle; the cross-rank energy
-terms must match the whole-grid terms.  The rank-0 ncclUniqueId broadcast
-of DeviceContext (device.make_nccl_id) is exercised for real.
+Two timings of every exchange are replayed -- data taken and delivered when
+the exchange starts ("eager") and when the program first waits for it
+("lazy") -- so a launch placed between an exchange and its wait that read
+the ghosts or wrote the faces would change the result.  Both must equal the
+single-process oracle bit for bit (fields) and to summation order (records).
+A mutated program (one wait removed) must fail, which shows the replay is
+sensitive to the schedule.  The rank-0 ncclUniqueId broadcast of
+DeviceContext (device.make_nccl_id) is exercised for real.
 """
 from __future__ import annotations
 
@@ -21,15 +30,17 @@ import socket
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2502_09537_b200 import GridSpec, PhysParams, seeded_random_state
+from paper_2502_09537_b200 import GridSpec, PhysParams, _lib, seeded_random_state
 from paper_2502_09537_b200.device import (_torch_allgather, _torch_broadcast,
                                           combine_rank_terms, make_nccl_id, slab_range)
 
 PARAMS = PhysParams(1.1, 0.9, 1.2, 0.8)
+OP_NONE, OP_BASE, OP_ADJ = 0, 1, 2
 
 
 def _free_port() -> int:
@@ -38,95 +49,149 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def exchange_faces(slab: dict, rank: int, world: int) -> None:
-    """Fill ghost planes 0 and -1 of every field from the neighbours, with the
-    order rule of kgs_host.cu:exchange(): sends [to dn: first plane, to up:
-    last plane], recvs [from up: ghost after, from dn: ghost before]."""
-    up, dn = (rank + 1) % world, (rank - 1) % world
-    for f in "PQUV":
-        a = slab[f]
-        first = np.ascontiguousarray(a[1])
-        last = np.ascontiguousarray(a[-2])
-        import torch
-        t_first, t_last = torch.from_numpy(first), torch.from_numpy(last)
-        r_after, r_before = torch.empty_like(t_first), torch.empty_like(t_first)
-        ops = [dist.P2POp(dist.isend, t_first, dn), dist.P2POp(dist.isend, t_last, up),
-               dist.P2POp(dist.irecv, r_after, up), dist.P2POp(dist.irecv, r_before, dn)]
+# ---- the per-point arithmetic (oracle.numpy_half_sweep, kernels.py:43-94) ----
+def _apply(op, P, Q, U, V, SP, SQ, SU, a):
+    alpha, beta, gcoef, c_uv, uv_nbr, gU, half_tau, i00, i01, i10, i11 = a
+
+    def psi(P, Q, Uc):
+        cr = gcoef * Uc - alpha
+        rr = -cr * P - Q - beta * SP
+        ri = P - cr * Q - beta * SQ
+        den = cr * cr + 1.0
+        return (rr * cr + ri) / den, (ri * cr - rr) / den
+
+    def uv(U, V, Pm, Qm):
+        r1 = U + half_tau * V
+        r2 = V - c_uv * U + uv_nbr * SU + gU * (Pm * Pm + Qm * Qm)
+        return i00 * r1 + i01 * r2, i10 * r1 + i11 * r2
+
+    if op == OP_BASE:
+        P, Q = psi(P, Q, U)
+        U, V = uv(U, V, P, Q)
+    elif op == OP_ADJ:
+        U, V = uv(U, V, P, Q)
+        P, Q = psi(P, Q, U)
+    return P, Q, U, V
+
+
+class SlabReplay:
+    """One rank's slab (natural layout, ghost planes at index 0 and nx+1)
+    executing kgs_step_program rows."""
+
+    def __init__(self, grid, state, rank, world, args, lazy):
+        self.g, self.rank, self.world, self.args, self.lazy = grid, rank, world, args, lazy
+        N = grid.N
+        self.x0, self.nx = slab_range(N, rank, world)
+        self.f = {}
+        for name in "PQUV":
+            a = getattr(state, name).reshape(grid.shape)
+            s = np.full((self.nx + 2, N, N), np.nan)
+            s[1:-1] = a[self.x0:self.x0 + self.nx]
+            self.f[name] = s
+        idx = np.indices((self.nx + 2, N, N))
+        self.parity = (idx[0] - 1 + self.x0 + idx[1] + idx[2]) % 2   # global parity per slot
+        self.pending = []          # exchanges started, not yet delivered (lazy)
+        self.acc = {0: np.zeros(8), 1: np.zeros(8)}
+        self.records = []
+        self.deferred = False
+        # ghosts as after an upload: both colours exchanged (V never: NaN)
+        for col in (0, 1):
+            self._exchange(col)
+
+    # -- exchange: only colour `col` values of P, Q, U travel ------------------
+    def _exchange(self, col):
+        up, dn = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        first = torch.from_numpy(np.stack([self.f[n][1] for n in "PQU"]).copy())
+        last = torch.from_numpy(np.stack([self.f[n][self.nx] for n in "PQU"]).copy())
+        from_up, from_dn = torch.empty_like(first), torch.empty_like(first)
+        ops = [dist.P2POp(dist.isend, first, dn, tag=1), dist.P2POp(dist.isend, last, up, tag=2),
+               dist.P2POp(dist.irecv, from_up, up, tag=1),
+               dist.P2POp(dist.irecv, from_dn, dn, tag=2)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-        a[-1] = r_after.numpy()
-        a[0] = r_before.numpy()
+        for gi, data in ((self.nx + 1, from_up.numpy()), (0, from_dn.numpy())):
+            m = self.parity[gi] == col
+            for k, n in enumerate("PQU"):
+                self.f[n][gi][m] = data[k][m]
+
+    # -- one launch: colour `col` over local planes [xa, xb) -------------------
+    def _launch(self, col, op1, op2, diag, xa, xb):
+        a, N = self.args, self.g.N
+        sl = slice(xa + 1, xb + 1)
+
+        def nsum(arr):     # canonical order -x, +x, -y, +y, -z, +z, seeded 0.0
+            s = np.zeros((xb - xa, N, N))
+            s = s + arr[xa:xb]
+            s = s + arr[xa + 2:xb + 2]
+            for ax in (1, 2):
+                s = s + np.roll(arr[sl], 1, axis=ax)
+                s = s + np.roll(arr[sl], -1, axis=ax)
+            return s
+
+        m = self.parity[sl] == col
+        SP, SQ, SU = (nsum(self.f[n])[m] for n in "PQU")
+        P, Q, U, V = (self.f[n][sl][m] for n in "PQUV")
+        after = 1 if op1 == OP_ADJ else (2 if op2 == OP_ADJ else 0)
+        P, Q, U, V = _apply(op1, P, Q, U, V, SP, SQ, SU, a)
+        if diag and after == 1:
+            self._measure(col, sl, m, P, Q, U, V)
+        P, Q, U, V = _apply(op2, P, Q, U, V, SP, SQ, SU, a)
+        if diag and after == 2:
+            self._measure(col, sl, m, P, Q, U, V)
+        for n, v in zip("PQUV", (P, Q, U, V)):
+            view = self.f[n][sl]
+            view[m] = v
+
+    def _measure(self, col, sl, m, P, Q, U, V):
+        """The fused record terms (DIAG): self terms of the colour's points;
+        red points also add their 2d incident edges (each edge joins one red
+        and one black point, so every edge is counted once)."""
+        t = self.acc[col]
+        pq = P * P + Q * Q
+        t[3] += np.sum(V * V)
+        t[4] += np.sum(U * U)
+        t[5] += np.sum(pq * U)
+        t[6] += np.sum(P * P)
+        t[7] += np.sum(Q * Q)
+        if col == 1:
+            lo, hi = sl.start, sl.stop
+            for q, (n, own) in enumerate(zip("PQU", (P, Q, U))):
+                arr = self.f[n]
+                nbs = [arr[lo - 1:hi - 1], arr[lo + 1:hi + 1]]
+                for ax in (1, 2):
+                    nbs += [np.roll(arr[sl], 1, axis=ax), np.roll(arr[sl], -1, axis=ax)]
+                for nb in nbs:
+                    t[q] += np.sum((nb[m] - own) ** 2)
+
+    def run(self, program):
+        for kind, col, op1, op2, diag, check, step, xa, xb in program.tolist():
+            if kind == _lib.PG_PASS_BEGIN:
+                if diag:
+                    self.acc[col] = np.zeros(8)
+            elif kind == _lib.PG_LAUNCH:
+                self._launch(col, op1, op2, diag, xa, xb)
+            elif kind == _lib.PG_XCH:
+                if self.lazy:
+                    self.pending.append(col)
+                else:
+                    self._exchange(col)
+            elif kind == _lib.PG_WAIT_XCH:
+                for c in self.pending:
+                    self._exchange(c)
+                self.pending = []
+            elif kind == _lib.PG_RECORD:
+                assert step == len(self.records)
+                self.records.append(self.acc[1] + (self.acc[0] if xa else 0.0))
+            elif kind == _lib.PG_DEFER:
+                self.deferred = True
+            elif kind == _lib.PG_PASS_END:
+                pass
+            else:
+                raise AssertionError(f"unknown program row kind {kind}")
+        assert not self.pending, "program ended with an exchange nobody waited for"
 
 
-def slab_half_sweep(slab: dict, args, grid: GridSpec, x0: int, colour: int,
-                    adjoint: bool) -> None:
-    """numpy_half_sweep on a slab with ghost planes (x neighbours from the
-    ghosts, y and z periodic) -- the same arithmetic as oracle/."""
-    alpha, beta, gcoef, c_uv, uv_nbr, gU, half_tau, i00, i01, i10, i11 = args
-    nx = slab["P"].shape[0] - 2
-    inner = (slice(1, nx + 1),)
-
-    def nsum(a):
-        s = np.zeros(a[1:-1].shape)
-        s = s + a[:-2]                                  # -x
-        s = s + a[2:]                                   # +x
-        for ax in (1, 2):
-            s = s + np.roll(a[1:-1], 1, axis=ax)
-            s = s + np.roll(a[1:-1], -1, axis=ax)
-        return s
-
-    SP, SQ, SU = (nsum(slab[f]) for f in "PQU")
-    idx = np.indices((nx, grid.N, grid.N))
-    m = ((idx[0] + x0 + idx[1] + idx[2]) % 2) == colour
-    P, Q, U, V = (slab[f][inner][m] for f in "PQUV")
-    SP, SQ, SU = SP[m], SQ[m], SU[m]
-    if not adjoint:
-        cr = gcoef * U - alpha
-        rr = -cr * P - Q - beta * SP
-        ri = P - cr * Q - beta * SQ
-        den = cr * cr + 1.0
-        Pn = (rr * cr + ri) / den
-        Qn = (ri * cr - rr) / den
-        r1 = U + half_tau * V
-        r2 = V - c_uv * U + uv_nbr * SU + gU * (Pn * Pn + Qn * Qn)
-        Un, Vn = i00 * r1 + i01 * r2, i10 * r1 + i11 * r2
-    else:
-        r1 = U + half_tau * V
-        r2 = V - c_uv * U + uv_nbr * SU + gU * (P * P + Q * Q)
-        Un, Vn = i00 * r1 + i01 * r2, i10 * r1 + i11 * r2
-        cr = gcoef * Un - alpha
-        rr = -cr * P - Q - beta * SP
-        ri = P - cr * Q - beta * SQ
-        den = cr * cr + 1.0
-        Pn = (rr * cr + ri) / den
-        Qn = (ri * cr - rr) / den
-    for f, v in zip("PQUV", (Pn, Qn, Un, Vn)):
-        view = slab[f][inner]
-        view[m] = v
-
-
-def slab_terms(slab: dict, grid: GridSpec) -> np.ndarray:
-    """This rank's 8 energy/mass term sums; forward x-edges of the last
-    plane use the ghost plane after it (each edge counted exactly once)."""
-    import math
-    t = np.zeros(8)
-    for q, f in enumerate("PQU"):
-        a = slab[f]
-        parts = [(a[2:] - a[1:-1]).ravel()]
-        for ax in (1, 2):
-            d = np.roll(a[1:-1], -1, axis=ax) - a[1:-1]
-            parts.append(d.ravel())
-        t[q] = math.fsum(np.concatenate(parts) ** 2)
-    P, Q, U, V = (slab[f][1:-1].ravel() for f in "PQUV")
-    t[3] = math.fsum(V * V)
-    t[4] = math.fsum(U * U)
-    t[5] = math.fsum((P * P + Q * Q) * U)
-    t[6] = math.fsum(P * P)
-    t[7] = math.fsum(Q * Q)
-    return t
-
-
-def _worker(rank: int, world: int, port: int, N: int, steps: int, out):
+def _worker(rank, world, port, N, calls, lazy, mutate, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -134,43 +199,140 @@ def _worker(rank: int, world: int, port: int, N: int, steps: int, out):
         ids = _torch_allgather(nid)
         grid = GridSpec(3, -1.0, 1.0, N)
         s = seeded_random_state(grid, 42, 0.5)
-        x0, nx = slab_range(N, rank, world)
-        slab = {}
-        for f in "PQUV":
-            a = getattr(s, f).reshape(grid.shape)
-            slab[f] = np.concatenate([a[(x0 - 1) % N][None], a[x0:x0 + nx],
-                                      a[(x0 + nx) % N][None]]).copy()
         args = oracle.kernel_args(PARAMS, 0.02, grid)
-        for _ in range(steps):
-            for colour, adj in ((1, False), (0, False), (0, True), (1, True)):
-                slab_half_sweep(slab, args, grid, x0, colour, adj)
-                exchange_faces(slab, rank, world)
-        terms = combine_rank_terms(_torch_allgather(slab_terms(slab, grid)))
-        out.put((rank, x0, {f: slab[f][1:-1].copy() for f in "PQUV"}, terms,
+        rep = SlabReplay(grid, s, rank, world, args, lazy)
+        offset, head_fused = 0, False
+        for nsteps, stride, defer in calls:
+            prog = _lib.step_program(rep.nx, True, nsteps, offset, stride, defer_tail=defer,
+                                     head_fused=head_fused)
+            if mutate:   # drop the first wait of every pass
+                keep, seen = [], False
+                for row in prog:
+                    if row[0] == _lib.PG_PASS_BEGIN:
+                        seen = False
+                    if row[0] == _lib.PG_WAIT_XCH and not seen:
+                        seen = True
+                        continue
+                    keep.append(row)
+                prog = np.array(keep)
+            rep.records = []
+            rep.run(prog)
+            head_fused, rep.deferred = rep.deferred, False
+            offset += nsteps
+        recs = [combine_rank_terms(_torch_allgather(r)) for r in rep.records]
+        out.put((rank, rep.x0, {n: rep.f[n][1:-1].copy() for n in "PQUV"}, recs,
                  len(set(ids)), len(nid)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,N", [(2, 8), (4, 8), (2, 6)])
-def test_slab_halo_protocol_bitwise(world, N):
-    steps = 3
+def _run_world(world, N, calls, lazy, mutate=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, N, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, calls, lazy, mutate, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    results = [q.get(timeout=240) for _ in range(world)]
+    results = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return sorted(results, key=lambda r: r[0])
+
+
+def _reference(N, total_steps, record_steps):
     grid = GridSpec(3, -1.0, 1.0, N)
     ref = seeded_random_state(grid, 42, 0.5)
-    oracle.numpy_step_dpavf2(ref, oracle.kernel_args(PARAMS, 0.02, grid), grid, steps)
+    args = oracle.kernel_args(PARAMS, 0.02, grid)
+    terms = {}
+    for n in range(1, total_steps + 1):
+        oracle.numpy_step_dpavf2(ref, args, grid, 1)
+        if n in record_steps:
+            terms[n] = oracle.energy_terms(ref, grid)
+    return grid, ref, terms
+
+
+# (nsteps, record_stride, defer_tail) per call; a deferred tail is fused
+# into the next call's head (KGS_PROGRAM_HEAD_FUSED), as on the device
+CASES = [
+    (2, 8, [(3, 1, False)]),                            # nx = 4, a record every step
+    (4, 8, [(2, 2, True), (2, 2, False)]),              # nx = 2: no interior launch
+    (2, 6, [(1, 0, True), (3, 3, True), (1, 1, False)]),
+    (4, 12, [(3, 3, False)]),
+]
+
+
+@pytest.mark.parametrize("lazy", [False, True], ids=["eager", "lazy"])
+@pytest.mark.parametrize("world,N,calls", CASES)
+def test_step_program_replayed_over_gloo_is_bitwise(world, N, calls, lazy):
+    results = _run_world(world, N, calls, lazy)
+    total = sum(n for n, _, _ in calls)
+    # record steps of each call (the deferred tail of a call records nothing:
+    # a deferring call never ends on a record step, see kgs_step_program)
+    rec_steps, off = [], 0
+    for n, stride, _ in calls:
+        rec_steps += [off + i for i in range(1, n + 1) if stride and (off + i) % stride == 0]
+        off += n
+    grid, ref, terms = _reference(N, total, set(rec_steps))
     full = {f: getattr(ref, f).reshape(grid.shape) for f in "PQUV"}
-    for rank, x0, fields, terms, n_ids, id_len in results:
+    last_recs = None
+    for rank, x0, fields, recs, n_ids, id_len in results:
         assert n_ids == 1 and id_len == 128           # one ncclUniqueId, everywhere
         for f in "PQUV":
             assert np.array_equal(fields[f], full[f][x0:x0 + fields[f].shape[0]]), (rank, f)
-        np.testing.assert_allclose(terms, oracle.energy_terms(ref, grid), rtol=1e-13)
+        last_recs = recs
+    # the records of the LAST call, summed over ranks in rank order
+    last_n, last_stride, _ = calls[-1]
+    off = total - last_n
+    want = [terms[off + i] for i in range(1, last_n + 1)
+            if last_stride and (off + i) % last_stride == 0]
+    assert len(last_recs) == len(want)
+    for got, w in zip(last_recs, want):
+        np.testing.assert_allclose(got, w, rtol=1e-12, atol=1e-300)
+
+
+def test_replay_detects_a_missing_wait():
+    """Sanity of the replay itself: without the wait before the boundary
+    planes, a lazily delivered exchange arrives too late and the fields are
+    no longer the oracle's."""
+    world, N, calls = 2, 8, [(2, 0, False)]
+    results = _run_world(world, N, calls, lazy=True, mutate=True)
+    grid, ref, _ = _reference(N, 2, set())
+    full = {f: getattr(ref, f).reshape(grid.shape) for f in "PQUV"}
+    same = all(np.array_equal(fields[f], full[f][x0:x0 + fields[f].shape[0]])
+               for _, x0, fields, _, _, _ in results for f in "PQUV")
+    assert not same
+
+
+def test_step_program_structure():
+    """The exported program's invariants (no ranks needed): every pass is
+    bracketed, boundary planes follow the wait, each colour pass is followed
+    by the exchange of its colour, records carry consecutive slots."""
+    prog = _lib.step_program(6, True, 4, 0, 2)
+    kinds = prog[:, 0].tolist()
+    assert kinds.count(_lib.PG_PASS_BEGIN) == kinds.count(_lib.PG_PASS_END) == 1 + 2 * 4
+    rec = prog[prog[:, 0] == _lib.PG_RECORD]
+    assert rec[:, 6].tolist() == [0, 1]
+    i = 0
+    while i < len(prog):
+        if prog[i, 0] == _lib.PG_PASS_BEGIN:
+            body = prog[i + 1:i + 5]
+            assert body[:, 0].tolist() == [_lib.PG_LAUNCH, _lib.PG_WAIT_XCH, _lib.PG_LAUNCH,
+                                           _lib.PG_LAUNCH]
+            assert body[0, 7:].tolist() == [1, 5] and body[2, 7:].tolist() == [0, 1]
+            assert body[3, 7:].tolist() == [5, 6]
+            assert prog[i + 5, 0] == _lib.PG_PASS_END
+            assert prog[i + 6, 0] == _lib.PG_XCH and prog[i + 6, 1] == prog[i, 1]
+            i += 7
+        else:
+            i += 1
+    # one slab: a single whole-slab launch per pass, no waits inside passes
+    one = _lib.step_program(6, False, 2, 0, 0)
+    launches = one[one[:, 0] == _lib.PG_LAUNCH]
+    assert (launches[:, 7] == 0).all() and (launches[:, 8] == 6).all()
+    # a deferred tail leaves the red adjoint out; the next call fuses it
+    d = _lib.step_program(6, False, 2, 0, 0, defer_tail=True)
+    assert d[-2, 0] == _lib.PG_DEFER
+    h = _lib.step_program(6, False, 1, 2, 0, head_fused=True)
+    assert h[1, 1:4].tolist() == [1, OP_ADJ, OP_BASE]

@@ -12,11 +12,13 @@ from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
 
 import paper_2502_09537_b200 as kgs
-from conftest import assert_bitwise
+from conftest import assert_bitwise, experimental_build
 from paper_2502_09537_b200.device import get_context
 
 pytestmark = pytest.mark.gpu
 SETTINGS = settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+# the fused one-march step exists only in the experimental build
+FUSED = st.booleans() if experimental_build() else st.just(False)
 
 
 def _state(g, seed):
@@ -64,7 +66,7 @@ def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plan
 @SETTINGS
 @given(N=st.sampled_from([64, 128]), slabs=st.sampled_from([2, 4]), steps=st.integers(1, 6),
        stride=st.integers(0, 3), seed=st.integers(0, 2**31), mirror=st.booleans(),
-       fused=st.booleans(), defer=st.booleans(), poison=st.one_of(st.none(), st.integers(0, 127)))
+       fused=FUSED, defer=st.booleans(), poison=st.one_of(st.none(), st.integers(0, 127)))
 def test_slab_variants_equal_one_slab(N, slabs, steps, stride, seed, mirror, fused, defer,
                                       poison):
     g = kgs.GridSpec(3, -6.0, 6.0, N)
@@ -105,7 +107,7 @@ OPS = st.lists(st.one_of(
 
 @SETTINGS
 @given(N=st.sampled_from([64, 128]), slabs=st.sampled_from([2, 4]), seed=st.integers(0, 2**31),
-       mirror=st.booleans(), fused=st.booleans(), ops=OPS)
+       mirror=st.booleans(), fused=FUSED, ops=OPS)
 def test_random_operation_sequences_slabs_vs_one(N, slabs, seed, mirror, fused, ops):
     """Any interleaving of multi-step calls (records, deferred tails), single
     sweeps, energy evaluations, partial plane uploads and full uploads gives

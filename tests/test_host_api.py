@@ -40,7 +40,8 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.kgs_abi_version() == 100
+    assert lib.kgs_abi_version() == 101
+    assert lib.kgs_build_flags() == 0   # the default library: no experimental code, no asserts
 
 
 def test_library_is_sm100a():
@@ -182,7 +183,9 @@ def test_executor_config_modes():
     assert isinstance(kgs.ExecutorConfig("serial").build(), kgs.SerialExecutor)
     assert kgs.ExecutorConfig("phased", 4).build().workers == 4
     ex = kgs.ExecutorConfig("cuda", 2).build()
-    assert isinstance(ex, kgs.CudaExecutor) and ex.devices == (0, 1)
+    assert isinstance(ex, kgs.CudaExecutor) and ex.nslabs == 2
+    # one slab per GPU when the library sees enough devices, else virtual slabs
+    assert ex.devices == ((0, 1) if _lib.device_count() >= 2 else (0,))
     with pytest.raises(ValueError):
         kgs.ExecutorConfig("gpu", 1)        # reference tests/test_executor.py:23-27
     with pytest.raises(ValueError):
@@ -296,6 +299,16 @@ def test_cuda_executor_config_uses_virtual_slabs_beyond_the_gpu_count(monkeypatc
     monkeypatch.setattr(exm, "_device_count", lambda: 8)
     ex = kgs.ExecutorConfig("cuda", 4).build()
     assert ex.devices == (0, 1, 2, 3) and ex.slabs_per_device == 1
+    monkeypatch.setattr(exm, "_device_count", lambda: 0)   # no driver: never phantom devices
+    ex = kgs.ExecutorConfig("cuda", 2).build()
+    assert ex.devices == (0,) and ex.slabs_per_device == 2
+
+
+def test_device_count_comes_from_the_library():
+    n = _lib.device_count()
+    assert n >= 0
+    from paper_2502_09537_b200 import executor as exm
+    assert exm._device_count() == n
 
 
 def test_one_call_path_only_takes_whole_grid_writable_float64():
@@ -343,3 +356,25 @@ def test_build_preset_slab_is_the_whole_grid_slice():
             assert np.array_equal(getattr(slab, f), getattr(whole, f)[lo * 1024:hi * 1024])
     with pytest.raises(ValueError):
         build_preset("ellipsoids3d", g, planes=(0, 33))
+
+
+def test_colour_order_of_foreign_schedules():
+    """The reference's UpdateSchedule objects carry their colour order in
+    their phases (ordering.py:130-146); reverse_schedule'd ones sweep black
+    first and must run black first here too."""
+    from types import SimpleNamespace as NS
+    from paper_2502_09537_b200.ordering import colour_order, is_reversed
+    g = kgs.GridSpec(3, -1.0, 1.0, 4)
+    par = np.indices(g.shape).sum(axis=0).ravel() % 2
+    red, black = np.nonzero(par == 1)[0], np.nonzero(par == 0)[0]
+    fwd = NS(strategy="checkerboard", phases=[NS(lanes=[red[:5], red[5:]]), NS(lanes=[black])])
+    rev = NS(strategy="checkerboard", phases=[NS(lanes=[black[::-1]]),
+                                              NS(lanes=[red[5:][::-1], red[:5][::-1]])])
+    assert colour_order(fwd, g) == (RED, BLACK) and not is_reversed(fwd, g)
+    assert colour_order(rev, g) == (BLACK, RED) and is_reversed(rev, g)
+    rank = np.empty(g.M, dtype=np.int64)
+    rank[np.concatenate([black, red])] = np.arange(g.M)
+    assert colour_order(NS(strategy="checkerboard", rank=rank), g) == (BLACK, RED)
+    ours = kgs.checkerboard_schedule(g)
+    assert colour_order(ours, g) == (RED, BLACK)
+    assert colour_order(kgs.reverse_schedule(ours), g) == (BLACK, RED)
