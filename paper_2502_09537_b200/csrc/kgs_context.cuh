@@ -4,13 +4,14 @@
 
 namespace {
 
-// march kernel variants (kgs_launch.cuh): MV0..MV3 tile shapes; the
-// clustered and producer-warp variants MV4..MV6 are experimental (slower,
-// DESIGN.md §5) and exist only in -DKGS_EXPERIMENTAL builds
+// march kernel variants (kgs_launch.cuh): MV0..MV12 tile shapes, ring
+// depths and rows per thread; the clustered and producer-warp variants
+// MV13..MV15 are experimental (slower) and exist only in
+// -DKGS_EXPERIMENTAL builds
 #ifdef KGS_EXPERIMENTAL
-constexpr int kMarchVariantSlots = 7;
+constexpr int kMarchVariantSlots = 16;
 #else
-constexpr int kMarchVariantSlots = 4;
+constexpr int kMarchVariantSlots = 13;
 #endif
 
 thread_local std::string g_last_error = "no error";
@@ -121,7 +122,7 @@ struct kgs_ctx {
   // tuning knobs (kgs_set_tuning): rows per tile, band height, blocks/SM cap
   int tune_ty = 4, tune_band_rows = 64, tune_occ = 0;
   int tune_xc = 0;  // march kernel planes per unit (0 auto, < 0 disables it)
-  int tune_variant = 0;  // march kernel tile variant (MV0..MV3)
+  int tune_variant = 4;  // march kernel variant (kgs_launch.cuh; MV4: 8 x 64 tiles, 2 rows per thread)
   int tune_promo_halo = 0, tune_promo_tile = 0;  // TMA L2 promotion (0 none .. 3 256B)
   int tune_sync = 4;     // march clusters: planes between cluster barriers
   // deferred tail (KGS_STEP_DEFER_TAIL): the red adjoint of the last step is

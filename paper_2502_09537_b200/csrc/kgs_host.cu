@@ -663,7 +663,8 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   Slab& s = ctx->slabs[0];
   PassGeom g = make_geom(ctx, s, 0, 0, s.nx);
   const int v = march_variant(ctx, s, g);
-  if (v != 0 && v != 4) return fail(ctx, KGS_EINVAL, "debug pass needs march variant 0 or 4");
+  if (v != 0 && v != 4 && v != 13)
+    return fail(ctx, KGS_EINVAL, "debug pass needs march variant 0, 4 or 13");
   if (int r0 = flush_pending(ctx)) return r0;
   Coeffs c{};
   CK(cudaSetDevice(s.dev));
@@ -676,12 +677,15 @@ int kgs_debug_pass(kgs_ctx* ctx, int mode, int reps, double* ms_out) {
   int r = KGS_OK;
   for (int i = 0; i <= reps && !r; ++i) {
     if (i == 1) CK(cudaEventRecord(a, s.stream));
-#define KGS_DBG(M)                                                                       \
-  r = (v == 0) ? launch_march<MV0, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v) \
-               : launch_march<MV4, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v);
+#define KGS_DBG(M)                                                                         \
+  r = (v == 0)   ? launch_march<MV0, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v)  \
+      : (v == 4) ? launch_march<MV4, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v)  \
+                 : launch_march<MV13, 0, OP_BASE, OP_ADJ, false, false, M>(ctx, s, g, c, 0, v);
     switch (mode) {
       case 0: KGS_DBG(0) break;
       case 1: KGS_DBG(1) break;
+      case 4: KGS_DBG(4) break;
+      case 5: KGS_DBG(5) break;
       default: KGS_DBG(3) break;
     }
 #undef KGS_DBG
@@ -737,7 +741,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   if (n == "march_sync") ctx->tune_sync = std::max(1, value);
   else if (n == "march_variant") {
     if (value >= kMarchVariantSlots)
-      return fail(ctx, KGS_EINVAL, "march_variant %d not in this build (0..%d; 4..6 need "
+      return fail(ctx, KGS_EINVAL, "march_variant %d not in this build (0..%d; 13..15 need "
                   "-DKGS_EXPERIMENTAL)", value, kMarchVariantSlots - 1);
     ctx->tune_variant = value;
   }

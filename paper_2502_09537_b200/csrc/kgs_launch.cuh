@@ -80,35 +80,54 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// 3-D march kernel variants: tile rows x slots, ring depths, min blocks/SM.
-// Larger tile cross-sections re-read fewer halo rows/slots.
-template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_, int CL_ = 1, bool PW_ = false>
+// 3-D march kernel variants: tile rows x slots, ring depths, min blocks/SM,
+// cluster size, producer warp, rows per thread.  Larger tile cross-sections
+// re-read fewer halo rows/slots; deeper rings keep more bytes in flight;
+// several rows per thread (RPT) interleave independent fp64 chains, so fewer
+// warps (hence more shared memory per CTA for the rings) keep the FP64 pipe
+// busy.
+template <int TY_, int TK_, int NOTH_, int NOWN_, int MINB_, int CL_ = 1, bool PW_ = false,
+          int RPT_ = 1>
 struct MarchVariant {
   static constexpr int TY = TY_, TK = TK_, NOTH = NOTH_, NOWN = NOWN_, MINB = MINB_, CL = CL_;
   static constexpr bool PW = PW_;
-  static constexpr int NT = TY * TK + (PW ? 32 : 0);   // + the producer warp
+  static constexpr int RPT = RPT_;
+  static constexpr int NT = TY * TK / RPT + (PW ? 32 : 0);   // + the producer warp
   using L = MarchSmem<TY, TK, NOTH, NOWN>;
 };
 using MV0 = MarchVariant<4, 64, 4, 2, 4>;     // 256 threads, 4 blocks/SM
 using MV1 = MarchVariant<8, 64, 4, 2, 2>;     // 512 threads, 2 blocks/SM
 using MV2 = MarchVariant<16, 32, 4, 2, 2>;    // 512 threads, 2 blocks/SM
 using MV3 = MarchVariant<32, 32, 4, 2, 1>;    // 1024 threads, 1 block/SM
+using MV4 = MarchVariant<8, 64, 4, 2, 2, 1, false, 2>;   // 256 threads x 2 rows, 2 blocks/SM
+using MV5 = MarchVariant<4, 64, 5, 3, 3, 1, false, 2>;   // 128 threads x 2 rows, deep rings, 3/SM
+using MV6 = MarchVariant<4, 64, 4, 2, 4, 1, false, 2>;   // 128 threads x 2 rows, 4 blocks/SM
+using MV7 = MarchVariant<16, 64, 4, 2, 1, 1, false, 2>;  // 512 threads x 2 rows, 1 block/SM
+using MV8 = MarchVariant<16, 64, 4, 2, 1, 1, false, 4>;  // 256 threads x 4 rows, 1 block/SM
+using MV9 = MarchVariant<16, 32, 4, 2, 2, 1, false, 2>;  // 256 threads x 2 rows, 2 blocks/SM
+using MV10 = MarchVariant<8, 128, 4, 2, 1, 1, false, 2>; // 512 threads x 2 rows, 1 block/SM
+using MV11 = MarchVariant<8, 32, 4, 2, 4, 1, false, 2>;  // 128 threads x 2 rows, 4 blocks/SM
+using MV12 = MarchVariant<8, 64, 5, 2, 2, 1, false, 2>;  // MV4 with one more other-colour plane
 constexpr int kMarchVariants = kMarchVariantSlots;
 #ifdef KGS_EXPERIMENTAL
-using MV4 = MarchVariant<4, 64, 4, 2, 4, 8>;  // MV0 in clusters of 8 along y
-using MV5 = MarchVariant<4, 64, 4, 2, 4, 4>;  // MV0 in clusters of 4 along y
-using MV6 = MarchVariant<4, 64, 4, 2, 4, 1, true>;  // MV0 + a producer warp, no block barrier
-constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY, MV4::TY, MV5::TY,
-                                        MV6::TY};
-constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK, MV4::TK, MV5::TK,
-                                        MV6::TK};
-constexpr int kVarCL[kMarchVariants] = {MV0::CL, MV1::CL, MV2::CL, MV3::CL, MV4::CL, MV5::CL,
-                                        MV6::CL};
+using MV13 = MarchVariant<4, 64, 4, 2, 4, 8>;  // MV0 in clusters of 8 along y
+using MV14 = MarchVariant<4, 64, 4, 2, 4, 4>;  // MV0 in clusters of 4 along y
+using MV15 = MarchVariant<4, 64, 4, 2, 4, 1, true>;  // MV0 + a producer warp, no block barrier
+#define KGS_MV_LIST(F) F(MV0), F(MV1), F(MV2), F(MV3), F(MV4), F(MV5), F(MV6), F(MV7), F(MV8), \
+                       F(MV9), F(MV10), F(MV11), F(MV12), F(MV13), F(MV14), F(MV15)
 #else
-constexpr int kVarTY[kMarchVariants] = {MV0::TY, MV1::TY, MV2::TY, MV3::TY};
-constexpr int kVarTK[kMarchVariants] = {MV0::TK, MV1::TK, MV2::TK, MV3::TK};
-constexpr int kVarCL[kMarchVariants] = {MV0::CL, MV1::CL, MV2::CL, MV3::CL};
+#define KGS_MV_LIST(F) F(MV0), F(MV1), F(MV2), F(MV3), F(MV4), F(MV5), F(MV6), F(MV7), F(MV8), \
+                       F(MV9), F(MV10), F(MV11), F(MV12)
 #endif
+#define KGS_MV_TY(V) V::TY
+#define KGS_MV_TK(V) V::TK
+#define KGS_MV_CL(V) V::CL
+constexpr int kVarTY[kMarchVariants] = {KGS_MV_LIST(KGS_MV_TY)};
+constexpr int kVarTK[kMarchVariants] = {KGS_MV_LIST(KGS_MV_TK)};
+constexpr int kVarCL[kMarchVariants] = {KGS_MV_LIST(KGS_MV_CL)};
+#undef KGS_MV_TY
+#undef KGS_MV_TK
+#undef KGS_MV_CL
 
 // L2 sector promotion of the TMA boxes.  The two-slot halo columns are 16 B
 // inside a neighbouring tile's lines: promoting them to 256-B fetches would
@@ -179,9 +198,12 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
                  int v) {
   using L = typename Var::L;
   constexpr int CL = Var::CL;
+  // record passes carry 8 more accumulators: one-point-per-thread variants
+  // give them half the blocks per SM (more registers, no spills); the
+  // two-rows-per-thread variants already run few, wide blocks and keep them
+  constexpr int kMinB = (DIAG && Var::RPT == 1) ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB;
   auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
-                         DIAG ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB, DBG, CL,
-                         Var::PW>;
+                         kMinB, DBG, CL, Var::PW, Var::RPT>;
   // resident CTAs per SM (or clusters per GPU / nsm when CL > 1), per device
   static int occ_dev[kMaxDevices] = {};
   static int max_clusters_dev[kMaxDevices] = {};
@@ -222,6 +244,7 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   mc.sync = std::max(1, ctx->tune_sync);
   const int64_t grid = std::min<int64_t>(mc.nunits, G) / CL * CL;
   if (grid < 1) return KGS_OK;
+
   if (CL > 1) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -318,15 +341,15 @@ template <int COL, int O1, int O2, bool DG, bool CH>
 int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
                      int v) {
   switch (v) {
-    case 0: return launch_march<MV0, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    case 1: return launch_march<MV1, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    case 2: return launch_march<MV2, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+#define KGS_MV_CASE(N) \
+    case N: return launch_march<MV##N, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    KGS_MV_CASE(0) KGS_MV_CASE(1) KGS_MV_CASE(2) KGS_MV_CASE(3) KGS_MV_CASE(4) KGS_MV_CASE(5)
+    KGS_MV_CASE(7) KGS_MV_CASE(8) KGS_MV_CASE(9) KGS_MV_CASE(10) KGS_MV_CASE(11) KGS_MV_CASE(12)
 #ifdef KGS_EXPERIMENTAL
-    case 4: return launch_march<MV4, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    case 5: return launch_march<MV5, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    case 6: return launch_march<MV6, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    KGS_MV_CASE(13) KGS_MV_CASE(14) KGS_MV_CASE(15)
 #endif
-    default: return launch_march<MV3, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+#undef KGS_MV_CASE
+    default: return launch_march<MV6, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
   }
 }
 

@@ -305,6 +305,7 @@ int reset_bad(kgs_ctx* ctx) {
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
     CK(cudaMemsetAsync(s.bad, 0xff, sizeof(unsigned long long), s.stream));
+
   }
   return KGS_OK;
 }
@@ -350,6 +351,7 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
   }
   CK(cudaMalloc(&s.bad, sizeof(unsigned long long)));
   CK(cudaMemset(s.bad, 0xff, sizeof(unsigned long long)));
+
   // staging: up to 256 MiB of natural-layout planes of one field
   const size_t nat_plane = (size_t)ctx->ny * ctx->nz * sizeof(double);
   s.stage_planes = (int)std::max<size_t>(1, std::min<size_t>(s.nx, (256u << 20) / nat_plane));

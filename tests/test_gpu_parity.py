@@ -284,14 +284,17 @@ _EXP = needs_experimental
 
 
 @pytest.mark.parametrize("variant,xc", [(1, 0), (1, 1), (1, 2), (1, 3), (1, 128), (0, 8), (2, 5), (3, 0),
-                                        pytest.param(4, 0, marks=_EXP), pytest.param(5, 3, marks=_EXP),
-                                        pytest.param(4, 16, marks=_EXP), pytest.param(6, 0, marks=_EXP),
-                                        pytest.param(6, 1, marks=_EXP), pytest.param(6, 5, marks=_EXP)])
+                                        (4, 0), (4, 3), (5, 0), (5, 1), (5, 7), (6, 0), (6, 2),
+                                        (7, 0), (7, 5), (8, 0), (8, 2), (9, 0), (9, 3), (10, 0),
+                                        (10, 6), (11, 0), (11, 1), (12, 0), (12, 4),
+                                        pytest.param(13, 0, marks=_EXP), pytest.param(14, 3, marks=_EXP),
+                                        pytest.param(13, 16, marks=_EXP), pytest.param(15, 0, marks=_EXP),
+                                        pytest.param(15, 1, marks=_EXP), pytest.param(15, 5, marks=_EXP)])
 def test_march_kernel_matches_simple_kernel(variant, xc):
     """3-D marching (TMA ring) kernel == simple per-point kernel, bitwise, for
     every tile variant and several work-unit sizes (incl. a non-divisor)."""
     sc = kgs.get_scenario("ellipsoids3d")
-    g = sc.default_grid(128)
+    g = sc.default_grid(256 if variant == 10 else 128)   # 8 x 128 tiles need 256 slots
     s0 = sc.state(g)
     args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
     outs = []
