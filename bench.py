@@ -47,7 +47,6 @@ METRIC = "3D KGS grid-point updates/s at 1/2/4/8 B200; % of HBM roofline vs CPU 
 UNIT = "point-updates/s"
 BYTES_PER_UPDATE = 64          # P,Q,U,V read+write once per update
 DESIGN_BYTES_PER_UPDATE = 44   # colour-split fused passes
-DIAG_STEPS = 5                # steps of the record-every-step run (diagnostics price)
 TAU = 0.01
 SCENARIO = "ellipsoids3d"
 
@@ -437,7 +436,7 @@ def run_ours(args):
 
     # price of the diagnostics (SURVEY.md §7 timed runs): a few more steps with
     # an energy/mass record after EVERY step, the reference's record_stride=1
-    R = DIAG_STEPS
+    R = K          # same step count as the timed run: same head/tail share
     barrier(world)
     terms_r, bad_r = ctx.step_dpavf2(kargs, R, W + K, 1)
     ms_r = max_over_ranks(ctx.last_step_ms(), world)

@@ -241,12 +241,11 @@ double kgs_last_step_ms(kgs_ctx* ctx);
  * rows for its band-major tile order (<= 0: plane-major), a cap on resident
  * blocks per SM (0: occupancy maximum), planes per work unit of the 3-D
  * marching kernel (0: automatic, < 0: never use the marching kernel), and
- * the marching kernel's tile variant (0: 4x64, 1: 8x64, 2: 16x32, 3: 32x32
- * rows x slots, one point per thread; 4: 8x64 with two rows per thread;
- * 5: 4x64, two rows per thread, deeper TMA rings (5 other / 3 own planes);
- * 6: 4x64, two rows per thread; experimental builds only: 7, 8: 4x64 in
- * clusters of 8 / 4 CTAs; 9: 4x64 with a producer warp and per-slot
- * release barriers instead of a block barrier per plane; < 0: keep).
+ * the marching kernel's variant (0: 4x64 rows x slots, one point per
+ * thread; 1: 8x64, one point per thread; 4, the default: 8x64, two rows per
+ * thread at 2 CTAs/SM; the other shapes 2, 3, 5..12 and the clustered /
+ * producer-warp variants 13..15 exist only in experimental builds; < 0:
+ * keep).
  * Results do not depend on these (bitwise). */
 int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_per_sm,
                    int march_planes, int march_variant);
@@ -316,7 +315,8 @@ int kgs_host_free(void* p);
 int kgs_abi_version(void);
 
 /* Build flags of this library: KGS_BUILD_EXPERIMENTAL (-DKGS_EXPERIMENTAL:
- * the slower fused one-march step, march variants 7..9 and kgs_debug_pass,
+ * the slower fused one-march step, march variants 2, 3, 5..15 and
+ * kgs_debug_pass,
  * kept for the DESIGN.md §5 measurements) and KGS_BUILD_CHECKED
  * (-DKGS_CHECKED: in-kernel index asserts).  The default library has
  * neither. */

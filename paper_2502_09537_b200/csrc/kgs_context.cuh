@@ -4,15 +4,10 @@
 
 namespace {
 
-// march kernel variants (kgs_launch.cuh): MV0..MV12 tile shapes, ring
-// depths and rows per thread; the clustered and producer-warp variants
-// MV13..MV15 are experimental (slower) and exist only in
-// -DKGS_EXPERIMENTAL builds
-#ifdef KGS_EXPERIMENTAL
+// march kernel variants (kgs_launch.cuh): MV0..MV15 (tile shapes, ring
+// depths, rows per thread, clusters, producer warp); the default build
+// compiles MV0, MV1 and MV4 (kVarBuilt), the others need -DKGS_EXPERIMENTAL
 constexpr int kMarchVariantSlots = 16;
-#else
-constexpr int kMarchVariantSlots = 13;
-#endif
 
 thread_local std::string g_last_error = "no error";
 

@@ -740,9 +740,9 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   const std::string n(name);
   if (n == "march_sync") ctx->tune_sync = std::max(1, value);
   else if (n == "march_variant") {
-    if (value >= kMarchVariantSlots)
-      return fail(ctx, KGS_EINVAL, "march_variant %d not in this build (0..%d; 13..15 need "
-                  "-DKGS_EXPERIMENTAL)", value, kMarchVariantSlots - 1);
+    if (value >= kMarchVariantSlots || (value >= 0 && !kVarBuilt[value]))
+      return fail(ctx, KGS_EINVAL, "march_variant %d not in this build (default build: 0, 1, "
+                  "4; the others need -DKGS_EXPERIMENTAL)", value);
     ctx->tune_variant = value;
   }
   else if (n == "march_planes") ctx->tune_xc = value;

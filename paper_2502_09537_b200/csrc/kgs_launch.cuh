@@ -108,16 +108,20 @@ using MV9 = MarchVariant<16, 32, 4, 2, 2, 1, false, 2>;  // 256 threads x 2 rows
 using MV10 = MarchVariant<8, 128, 4, 2, 1, 1, false, 2>; // 512 threads x 2 rows, 1 block/SM
 using MV11 = MarchVariant<8, 32, 4, 2, 4, 1, false, 2>;  // 128 threads x 2 rows, 4 blocks/SM
 using MV12 = MarchVariant<8, 64, 5, 2, 2, 1, false, 2>;  // MV4 with one more other-colour plane
-constexpr int kMarchVariants = kMarchVariantSlots;
-#ifdef KGS_EXPERIMENTAL
 using MV13 = MarchVariant<4, 64, 4, 2, 4, 8>;  // MV0 in clusters of 8 along y
 using MV14 = MarchVariant<4, 64, 4, 2, 4, 4>;  // MV0 in clusters of 4 along y
 using MV15 = MarchVariant<4, 64, 4, 2, 4, 1, true>;  // MV0 + a producer warp, no block barrier
+constexpr int kMarchVariants = kMarchVariantSlots;
 #define KGS_MV_LIST(F) F(MV0), F(MV1), F(MV2), F(MV3), F(MV4), F(MV5), F(MV6), F(MV7), F(MV8), \
                        F(MV9), F(MV10), F(MV11), F(MV12), F(MV13), F(MV14), F(MV15)
+// Variants compiled into this build: the default library carries MV4 (the
+// default), MV0 (one point per thread, the round-1 kernel) and MV1 (8 x 64,
+// one point per thread); every other shape was measured slower (DESIGN.md
+// §5) and exists only in -DKGS_EXPERIMENTAL builds.
+#ifdef KGS_EXPERIMENTAL
+constexpr bool kVarBuilt[kMarchVariants] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
 #else
-#define KGS_MV_LIST(F) F(MV0), F(MV1), F(MV2), F(MV3), F(MV4), F(MV5), F(MV6), F(MV7), F(MV8), \
-                       F(MV9), F(MV10), F(MV11), F(MV12)
+constexpr bool kVarBuilt[kMarchVariants] = {1, 1, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 #define KGS_MV_TY(V) V::TY
 #define KGS_MV_TK(V) V::TK
@@ -155,8 +159,8 @@ int make_maps_for(kgs_ctx* ctx, Slab& s, double* const bufs[2],
   const cuuint32_t es[4] = {1, 1, 1, 1};
   for (int v = 0; v < kMarchVariants; ++v) {
     const int ty = kVarTY[v], tk = kVarTK[v];
-    s.has_tmaps[v] = ctx->d == 3 && ctx->ny % (ty * kVarCL[v]) == 0 && ctx->nk % tk == 0 &&
-                     ctx->nk >= 2 && (ctx->rs * 8) % 16 == 0;
+    s.has_tmaps[v] = kVarBuilt[v] && ctx->d == 3 && ctx->ny % (ty * kVarCL[v]) == 0 &&
+                     ctx->nk % tk == 0 && ctx->nk >= 2 && (ctx->rs * 8) % 16 == 0;
     if (!s.has_tmaps[v]) continue;
     const cuuint32_t centre[4] = {(cuuint32_t)tk, 3, (cuuint32_t)ty, 1};
     const cuuint32_t row[4] = {(cuuint32_t)tk, 3, 1, 1};
@@ -343,13 +347,14 @@ int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, 
   switch (v) {
 #define KGS_MV_CASE(N) \
     case N: return launch_march<MV##N, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
-    KGS_MV_CASE(0) KGS_MV_CASE(1) KGS_MV_CASE(2) KGS_MV_CASE(3) KGS_MV_CASE(4) KGS_MV_CASE(5)
-    KGS_MV_CASE(7) KGS_MV_CASE(8) KGS_MV_CASE(9) KGS_MV_CASE(10) KGS_MV_CASE(11) KGS_MV_CASE(12)
+    KGS_MV_CASE(0) KGS_MV_CASE(1)
 #ifdef KGS_EXPERIMENTAL
-    KGS_MV_CASE(13) KGS_MV_CASE(14) KGS_MV_CASE(15)
+    KGS_MV_CASE(2) KGS_MV_CASE(3) KGS_MV_CASE(5) KGS_MV_CASE(6) KGS_MV_CASE(7) KGS_MV_CASE(8)
+    KGS_MV_CASE(9) KGS_MV_CASE(10) KGS_MV_CASE(11) KGS_MV_CASE(12) KGS_MV_CASE(13)
+    KGS_MV_CASE(14) KGS_MV_CASE(15)
 #endif
 #undef KGS_MV_CASE
-    default: return launch_march<MV6, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    default: return launch_march<MV4, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
   }
 }
 

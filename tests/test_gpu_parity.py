@@ -283,13 +283,15 @@ def test_shared_reciprocal_division():
 _EXP = needs_experimental
 
 
-@pytest.mark.parametrize("variant,xc", [(1, 0), (1, 1), (1, 2), (1, 3), (1, 128), (0, 8), (2, 5), (3, 0),
-                                        (4, 0), (4, 3), (5, 0), (5, 1), (5, 7), (6, 0), (6, 2),
-                                        (7, 0), (7, 5), (8, 0), (8, 2), (9, 0), (9, 3), (10, 0),
-                                        (10, 6), (11, 0), (11, 1), (12, 0), (12, 4),
-                                        pytest.param(13, 0, marks=_EXP), pytest.param(14, 3, marks=_EXP),
-                                        pytest.param(13, 16, marks=_EXP), pytest.param(15, 0, marks=_EXP),
-                                        pytest.param(15, 1, marks=_EXP), pytest.param(15, 5, marks=_EXP)])
+_DEFAULT_VARIANTS = [(1, 0), (1, 1), (1, 2), (1, 3), (1, 128), (0, 8), (0, 1), (4, 0), (4, 3),
+                     (4, 1), (4, 64)]
+_EXP_VARIANTS = [(2, 5), (3, 0), (5, 0), (5, 1), (5, 7), (6, 0), (6, 2), (7, 0), (7, 5), (8, 0),
+                 (8, 2), (9, 0), (9, 3), (10, 0), (10, 6), (11, 0), (11, 1), (12, 0), (12, 4),
+                 (13, 0), (14, 3), (13, 16), (15, 0), (15, 1), (15, 5)]
+
+
+@pytest.mark.parametrize("variant,xc", _DEFAULT_VARIANTS + [pytest.param(*v, marks=_EXP)
+                                                            for v in _EXP_VARIANTS])
 def test_march_kernel_matches_simple_kernel(variant, xc):
     """3-D marching (TMA ring) kernel == simple per-point kernel, bitwise, for
     every tile variant and several work-unit sizes (incl. a non-divisor)."""
