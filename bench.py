@@ -472,6 +472,24 @@ def run_ours(args):
                "note": "integrate(host page-locked FieldState): upload + K steps + download in "
                        "one call (pipelined on one slab: chunks stream in, passes follow as a "
                        "wavefront, finished chunks stream out); one untimed warm-up call first"}
+        # the same call on ordinary (pageable) numpy arrays -- what a dpavf
+        # user passes (grid.py:82-103): page-locked just in time inside the call
+        if host_memory_ok(2 * local_bytes, L):
+            plain = kgs.FieldState(*(np.array(getattr(host, f)) for f in "PQUV"), host.t)
+            # untimed warm-up call: allocates the page-locked staging slots
+            kgs.integrate(plain, g, sc.params, sch, ex, TAU, W * TAU, record_stride=W)
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            kgs.integrate(plain, g, sc.params, sch, ex, TAU, K * TAU, record_stride=K)
+            torch.cuda.synchronize()
+            pw = max_over_ranks(time.perf_counter() - t0, world)
+            e2e["pageable"] = {"value": updates / pw, "unit": UNIT, "wall_s": pw,
+                               "vs_pinned": e2e_wall / pw,
+                               "note": "integrate() on pageable numpy arrays (the reference's "
+                                       "FieldState), staged through page-locked slots by host "
+                                       "threads inside the call; one untimed warm-up call first"}
+            del plain
         kgs.clear_contexts()
     gpus_used = L.describe()
     barrier(world)

@@ -93,6 +93,9 @@ struct Slab {
   double* pipe_part = nullptr;      // per-record DIAG partials
   int64_t pipe_part_cap = 0;
   std::vector<cudaEvent_t> pipe_ev; // arrival / final events per chunk
+  double* hslot = nullptr;          // page-locked host slots for pageable arrays
+  int64_t hslot_len = 0;            // doubles per slot
+  std::vector<cudaEvent_t> hslot_ev;  // last DMA of each slot
 };
 
 }  // namespace
@@ -110,7 +113,7 @@ struct kgs_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   std::string err = "no error";
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};   // our kernel launches (the pipeline uploader thread adds too)
   double last_ms = 0.0;
   int nsm = 148;
   int grid_cap = 0;  // max persistent grid (blocks), sizes partials
@@ -131,7 +134,8 @@ struct kgs_ctx {
   int tune_tstore = 2;
   int tune_pdl = 1;          // colour passes: programmatic dependent launch
   int tune_pipe = 1;         // kgs_integrate_host: overlap upload | passes | download
-  int tune_pipe_chunk = 32;  // planes per transfer chunk     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
+  int tune_pipe_chunk = 32;  // planes per transfer chunk
+  int tune_stage = 1;        // kgs_integrate_host: stage pageable host arrays via page-locked slots     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
   // fused halo exchange (single-process slabs): boundary launches
   // store their faces straight into the neighbours' ghost planes
   bool mirror = false;       // possible for this context (peer-accessible neighbours)

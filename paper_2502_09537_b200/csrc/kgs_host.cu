@@ -11,10 +11,17 @@
 #include "kgs_device.cuh"
 
 #include <dlfcn.h>
+#include <immintrin.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <climits>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -62,7 +69,7 @@ const char* kgs_last_error(kgs_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_last_error.c_str();
 }
 
-int64_t kgs_launch_count(kgs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t kgs_launch_count(kgs_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 double kgs_last_step_ms(kgs_ctx* ctx) { return ctx ? ctx->last_ms : 0.0; }
 
@@ -197,6 +204,8 @@ int kgs_destroy(kgs_ctx* ctx) {
       if (s.ev_face[i]) cudaEventDestroy(s.ev_face[i]);
     if (s.dstream) cudaStreamSynchronize(s.dstream);
     for (auto e : s.pipe_ev) cudaEventDestroy(e);
+    for (auto e : s.hslot_ev) cudaEventDestroy(e);
+    if (s.hslot) cudaFreeHost(s.hslot);
     if (s.dstream) cudaStreamDestroy(s.dstream);
     if (s.pipe_up) cudaFree(s.pipe_up);
     if (s.pipe_dn) cudaFree(s.pipe_dn);
@@ -759,6 +768,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "tma_store") ctx->tune_tstore = value;
   else if (n == "pipeline") ctx->tune_pipe = value;
   else if (n == "pipeline_planes") ctx->tune_pipe_chunk = std::max(1, value);
+  else if (n == "stage_pageable") ctx->tune_stage = value;
   else if (n == "mirror_halo") ctx->tune_mirror = value;
   else if (n == "pdl") ctx->tune_pdl = value;
   else return fail(ctx, KGS_EINVAL, "unknown tuning parameter '%s'", name);

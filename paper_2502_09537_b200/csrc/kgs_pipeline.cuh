@@ -145,6 +145,98 @@ std::vector<int> pipeline_shrinks(int64_t nsteps) {
   return sh;
 }
 
+// ---- pageable host arrays: page-locked bounce slots ---------------------
+// The reference's FieldState holds ordinary numpy arrays (grid.py:82-103):
+// pageable memory, which cudaMemcpyAsync copies through a small driver
+// buffer synchronously (~11 GB/s measured), and page-locking them in place
+// (cudaHostRegister) runs at only 6-14 GB/s and does not scale with threads
+// (tools/pageable_probe.py).  So for pageable arrays the
+// pipeline stages every chunk through page-locked slots of its own: an
+// uploader thread copies chunk m into an upload slot with a team of host
+// threads and queues the DMA from it; a downloader thread copies each
+// finished block out of a download slot once its DMA has landed.  The
+// device side (arrival events, passes, merges) is unchanged.
+constexpr int kUpSlots = 2, kDnSlots = 3;
+
+bool host_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Copy with non-temporal (streaming) stores: the destination is not read
+// for ownership, so a staged byte costs one host-memory read and one write
+// instead of two reads and a write (host bandwidth is the bottleneck of a
+// staged transfer: every byte is also read or written once more by the DMA).
+__attribute__((target("avx512f"))) void stream_copy_avx512(char* dst, const char* src,
+                                                           size_t n) {
+  size_t head = (64 - ((uintptr_t)dst & 63)) & 63;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  const size_t body = n & ~(size_t)255;
+  for (size_t i = 0; i < body; i += 256) {
+    const __m512i a = _mm512_loadu_si512((const void*)(src + i));
+    const __m512i b = _mm512_loadu_si512((const void*)(src + i + 64));
+    const __m512i c = _mm512_loadu_si512((const void*)(src + i + 128));
+    const __m512i d = _mm512_loadu_si512((const void*)(src + i + 192));
+    _mm512_stream_si512((__m512i*)(dst + i), a);
+    _mm512_stream_si512((__m512i*)(dst + i + 64), b);
+    _mm512_stream_si512((__m512i*)(dst + i + 128), c);
+    _mm512_stream_si512((__m512i*)(dst + i + 192), d);
+  }
+  _mm_sfence();
+  std::memcpy(dst + body, src + body, n - body);
+}
+
+void stream_copy(char* dst, const char* src, size_t n) {
+  static const bool avx512 = __builtin_cpu_supports("avx512f");
+  if (avx512 && n >= 4096) stream_copy_avx512(dst, src, n);
+  else std::memcpy(dst, src, n);
+}
+
+// stream_copy with `threads` host threads (page-sized parts)
+void par_copy(char* dst, const char* src, size_t n, int threads) {
+  if (threads <= 1 || n < ((size_t)8 << 20)) {
+    stream_copy(dst, src, n);
+    return;
+  }
+  const size_t part = ((n + threads - 1) / threads + 4095) & ~(size_t)4095;
+  std::vector<std::thread> th;
+  for (int t = 0; t < threads; ++t) {
+    const size_t lo = (size_t)t * part;
+    if (lo >= n) break;
+    th.emplace_back([=] { stream_copy(dst + lo, src + lo, std::min(part, n - lo)); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// Page-locked slots of `slot` doubles each (cached in the slab).
+int ensure_host_slots(kgs_ctx* ctx, Slab& s, int64_t slot) {
+  const int n = kUpSlots + kDnSlots;
+  if (s.hslot && s.hslot_len >= slot) return KGS_OK;
+  if (s.hslot) cudaFreeHost(s.hslot);
+  s.hslot = nullptr;
+  s.hslot_len = 0;
+  if (cudaHostAlloc(&s.hslot, (size_t)(n * slot) * 8, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    s.hslot = nullptr;
+    return KGS_ENOMEM;
+  }
+  s.hslot_len = slot;
+  while ((int)s.hslot_ev.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s.hslot_ev.push_back(e);
+  }
+  return KGS_OK;
+}
+
 int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, int64_t nsteps,
                         int64_t step_offset, int64_t record_stride, int64_t nrec,
                         unsigned long long* bad_out) {
@@ -237,14 +329,50 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     return rr;
   };
 
+  // pageable arrays (the reference's numpy FieldState): stage through
+  // page-locked slots; page-locked arrays (FieldState.pinned) go direct
+  bool staged = false;
+  if (ctx->tune_stage)
+    for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
+  if (staged && ensure_host_slots(ctx, s, stage) != KGS_OK) staged = false;
+  // host threads per direction (uploads and downloads copy concurrently)
+  const int cp_threads = std::max(1, std::min(8, ((int)std::thread::hardware_concurrency() - 2) / 2));
+  auto up_slot = [&](int64_t m) { return s.hslot + (m % kUpSlots) * stage; };
+  // KGS_PIPE_DEBUG=1: host-side time breakdown of a staged call on stderr
+  static const bool dbg = std::getenv("KGS_PIPE_DEBUG") != nullptr;
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
+  const clk::time_point t_call = clk::now();
+  double up_wait = 0, up_copy = 0, dn_wait = 0, dn_copy = 0, main_wait_up = 0, main_wait_dn = 0;
+  auto dn_slot = [&](int64_t j) { return s.hslot + (kUpSlots + j % kDnSlots) * stage; };
+
   CK(cudaEventRecord(s.ev_t0, s.cstream));
   // uploads (folded block order) on the comm stream: H2D, split, backup copy
-  for (const PipeEvent& e : plan) {
-    if (e.kind != PIPE_ARRIVE) continue;
+  auto upload_chunk = [&](const PipeEvent& e) -> int {
     const int64_t m = e.pass, x0 = e.a, x1 = e.b, nxc = x1 - x0;
-    for (int f = 0; f < 4; ++f)
-      CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + x0 * nat_plane,
-                         (size_t)nxc * nat_plane * 8, cudaMemcpyHostToDevice, s.cstream));
+    const size_t bytes = (size_t)nxc * nat_plane * 8;
+    if (staged) {
+      cudaEvent_t done = s.hslot_ev[m % kUpSlots];
+      const clk::time_point t0 = clk::now();
+      if (m >= kUpSlots) CK(cudaEventSynchronize(done));   // the slot's last DMA has read it
+      const clk::time_point t1 = clk::now();
+      double* sl = up_slot(m);
+      for (int f = 0; f < 4; ++f)
+        par_copy((char*)(sl + f * C * nat_plane), (const char*)(host[f] + x0 * nat_plane), bytes,
+                 cp_threads);
+      up_wait += secs(t0, t1);
+      up_copy += secs(t1, clk::now());
+      for (int f = 0; f < 4; ++f)
+        CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, sl + f * C * nat_plane, bytes,
+                           cudaMemcpyHostToDevice, s.cstream));
+      CK(cudaEventRecord(done, s.cstream));
+    } else {
+      for (int f = 0; f < 4; ++f)
+        CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + x0 * nat_plane, bytes,
+                           cudaMemcpyHostToDevice, s.cstream));
+    }
     const int64_t cnt = nxc * ctx->ny * ctx->nk;
     const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
     for (int f = 0; f < 4; ++f) {
@@ -260,24 +388,121 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       CK(cudaMemcpyAsync(s.alt0[cc] + x0 * ctx->ps, s.plane0[cc] + x0 * ctx->ps,
                          (size_t)nxc * ctx->ps * 8, cudaMemcpyDeviceToDevice, s.cstream));
     CK(cudaEventRecord(s.pipe_ev[m], s.cstream));
+    return KGS_OK;
+  };
+
+  // staged: an uploader thread stages and queues the chunks (the passes
+  // below wait, host side, until a chunk's arrival event is recorded before
+  // queueing a wait on it); a downloader thread empties the download slots
+  std::mutex mu;
+  std::condition_variable cv;
+  int64_t arrived = 0;          // chunks whose arrival event is recorded
+  int err = KGS_OK;             // first error of a helper thread
+  struct DlJob { int64_t b0, nxc, j; };
+  std::vector<DlJob> dl_queue;  // download slot jobs, in issue order
+  size_t dl_next = 0;           // next job for the downloader
+  int64_t dl_done = 0;          // jobs whose host copy finished
+  bool dl_close = false;
+  std::thread uploader, downloader;
+  if (staged) {
+    uploader = std::thread([&] {
+      cudaSetDevice(s.dev);
+      for (const PipeEvent& e : plan) {
+        if (e.kind != PIPE_ARRIVE) continue;
+        const int rc = upload_chunk(e);
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (rc && !err) err = rc;
+          arrived = e.pass + 1;
+        }
+        cv.notify_all();
+        if (rc) break;
+      }
+    });
+    downloader = std::thread([&] {
+      cudaSetDevice(s.dev);
+      for (;;) {
+        DlJob jb;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return dl_next < dl_queue.size() || dl_close; });
+          if (dl_next >= dl_queue.size()) return;
+          jb = dl_queue[dl_next++];
+        }
+        const clk::time_point t0 = clk::now();
+        int rc = cudaEventSynchronize(s.hslot_ev[kUpSlots + jb.j % kDnSlots]) == cudaSuccess
+                     ? KGS_OK : fail(ctx, KGS_ECUDA, "download slot event failed");
+        const clk::time_point t1 = clk::now();
+        if (!rc) {
+          const double* sl = dn_slot(jb.j);
+          for (int f = 0; f < 4; ++f)
+            par_copy((char*)(host[f] + jb.b0 * nat_plane), (const char*)(sl + f * C * nat_plane),
+                     (size_t)jb.nxc * nat_plane * 8, cp_threads);
+        }
+        dn_wait += secs(t0, t1);
+        dn_copy += secs(t1, clk::now());
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (rc && !err) err = rc;
+          ++dl_done;
+        }
+        cv.notify_all();
+      }
+    });
+  } else {
+    for (const PipeEvent& e : plan) {
+      if (e.kind != PIPE_ARRIVE) continue;
+      if (int rc = upload_chunk(e)) return rc;
+    }
   }
+  // join the helper threads on every exit path
+  struct Joiner {
+    std::thread& up;
+    std::thread& dn;
+    std::mutex& mu;
+    std::condition_variable& cv;
+    bool& close;
+    ~Joiner() {
+      if (up.joinable()) up.join();
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        close = true;
+      }
+      cv.notify_all();
+      if (dn.joinable()) dn.join();
+    }
+  } joiner{uploader, downloader, mu, cv, dl_close};
 
   // the wavefront on the compute stream; downloads behind it
   int64_t ndl = 0;
   for (const PipeEvent& e : plan) {
     if (r) break;
     if (e.kind == PIPE_ARRIVE) {
+      if (staged) {
+        const clk::time_point t0 = clk::now();
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return arrived > e.pass || err != KGS_OK; });
+        main_wait_up += secs(t0, clk::now());
+        if (err) return err;
+      }
       CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[e.pass], 0));
     } else if (e.kind == PIPE_PASS) {
       r = launch_range(passes[e.pass], e.a, e.b);
     } else {
       const int64_t k = e.pass, b0 = e.a, nxc = e.b - e.a;
-      ++ndl;
+      const int64_t j = ndl++;
       cudaEvent_t ev = s.pipe_ev[nb + k];
       CK(cudaEventRecord(ev, s.stream));
       CK(cudaStreamWaitEvent(s.dstream, ev, 0));
       const int64_t cnt = nxc * ctx->ny * ctx->nk;
       const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
+      if (staged) {   // the download slot must have been emptied by the downloader
+        const clk::time_point t0 = clk::now();
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return dl_done >= j - kDnSlots + 1 || err != KGS_OK; });
+        main_wait_dn += secs(t0, clk::now());
+        if (err) return err;
+      }
       for (int f = 0; f < 4; ++f) {
         PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
         g.own += f * ctx->pp;
@@ -285,11 +510,31 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
         merge_field<<<blocks, 256, 0, s.dstream>>>(s.pipe_dn + f * C * nat_plane, g, (int)nxc,
                                                     (int)b0);
         ctx->launches++;
-        CK(cudaMemcpyAsync(host[f] + b0 * nat_plane, s.pipe_dn + f * C * nat_plane,
-                           (size_t)nxc * nat_plane * 8, cudaMemcpyDeviceToHost, s.dstream));
+        double* to = staged ? dn_slot(j) + f * C * nat_plane : host[f] + b0 * nat_plane;
+        CK(cudaMemcpyAsync(to, s.pipe_dn + f * C * nat_plane, (size_t)nxc * nat_plane * 8,
+                           cudaMemcpyDeviceToHost, s.dstream));
       }
       CK(cudaGetLastError());
+      if (staged) {
+        CK(cudaEventRecord(s.hslot_ev[kUpSlots + j % kDnSlots], s.dstream));
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          dl_queue.push_back({b0, nxc, j});
+        }
+        cv.notify_all();
+      }
     }
+  }
+  if (staged && !r) {   // every block copied out of its slot
+    const clk::time_point t0 = clk::now();
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return dl_done >= ndl || err != KGS_OK; });
+    if (dbg)
+      std::fprintf(stderr, "[kgs pipe] staged call %.3f s: uploader wait %.3f copy %.3f | "
+                   "downloader wait %.3f copy %.3f | main wait up %.3f dn %.3f tail %.3f\n",
+                   secs(t_call, clk::now()), up_wait, up_copy, dn_wait, dn_copy, main_wait_up,
+                   main_wait_dn, secs(t0, clk::now()));
+    if (err) return err;
   }
   if (r) return r;
   if (ndl != nb) return fail(ctx, KGS_ECUDA, "pipeline copied back %lld of %lld blocks",

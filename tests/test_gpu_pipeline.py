@@ -178,3 +178,39 @@ def test_pipeline_with_pinned_host_arrays(N, steps, stride, planes, poison):
     assert_bitwise(a, b, equal_nan=True)
     if ea is not None:
         np.testing.assert_allclose(ea, eb, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("N,steps,stride,planes,poison", [
+    (256, 6, 3, 32, None), (256, 5, 1, 7, None), (512, 4, 2, 32, None), (256, 3, 3, 16, 77)])
+def test_pipeline_pageable_arrays_staged(N, steps, stride, planes, poison):
+    """Ordinary (pageable) numpy arrays -- the reference's FieldState -- go
+    through page-locked host slots filled / emptied by helper threads while
+    the pipeline runs (knob stage_pageable); bitwise the direct pageable
+    copies and the page-locked-array path, incl. the non-finite replay, and
+    repeatable (a second staged call reuses the slots)."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(N)
+    s0 = sc.state(g)
+    if poison is not None:
+        s0.V[poison * N * N + 5] = np.nan
+    outs = []
+    for pin, pinned in ((1, False), (0, False), (1, True), (1, False)):
+        ctx = get_context(g, None)
+        ctx.set_param("pipeline_planes", planes)
+        ctx.set_param("stage_pageable", pin)
+        s = _pinned_copy(g, s0) if pinned else s0.copy()
+        try:
+            tr = kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, 0.01,
+                               steps * 0.01, record_stride=stride)
+            res = (tr.energy, None)
+        except FloatingPointError as e:
+            res = (None, str(e))
+        outs.append((s.copy(), res))
+    ctx.set_param("stage_pageable", 1)
+    ctx.set_param("pipeline_planes", 32)
+    a, (ea, xa) = outs[0]
+    for b, (eb, xb) in outs[1:]:
+        assert xa == xb
+        assert_bitwise(a, b, equal_nan=True)
+        if ea is not None:
+            np.testing.assert_allclose(ea, eb, rtol=1e-13, atol=0)
