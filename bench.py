@@ -436,16 +436,29 @@ def run_ours(args):
 
     # price of the diagnostics (SURVEY.md §7 timed runs): a few more steps with
     # an energy/mass record after EVERY step, the reference's record_stride=1
-    R = K          # same step count as the timed run: same head/tail share
-    barrier(world)
-    terms_r, bad_r = ctx.step_dpavf2(kargs, R, W + K, 1)
-    ms_r = max_over_ranks(ctx.last_step_ms(), world)
-    if bad_r:
-        raise FloatingPointError(f"non-finite state at step {bad_r}")
-    em = [kgs.grid.energy_from_terms(t, sc.params, g) for t in [terms[-1], *terms_r]]
-    diag = {"record_stride": 1, "steps": R, "ms_per_step": ms_r / R,
-            "value": 2.0 * g.M * R / (ms_r / 1e3), "unit": UNIT,
-            "cost_vs_unrecorded": (ms_r / R) / (ms / K),
+    # Interleaved blocks of B steps, recording every step or not at all, so
+    # clock / power drift over the run hits both alike; cost = ratio of the
+    # median block times (same step count, same head/tail share).
+    B, pairs = 10, 4
+    off = W + K
+    rec_ms, plain_ms, recs = [], [], [terms[-1]]
+    for _ in range(pairs):
+        for rec in (True, False):
+            barrier(world)
+            t_b, bad_b = ctx.step_dpavf2(kargs, B, off, 1 if rec else 0)
+            off += B
+            if bad_b:
+                raise FloatingPointError(f"non-finite state at step {bad_b}")
+            (rec_ms if rec else plain_ms).append(max_over_ranks(ctx.last_step_ms(), world) / B)
+            if rec:
+                recs.extend(t_b)
+    em = [kgs.grid.energy_from_terms(t, sc.params, g) for t in recs]
+    ms_rec, ms_plain = float(np.median(rec_ms)), float(np.median(plain_ms))
+    diag = {"record_stride": 1, "steps": B * pairs, "ms_per_step": ms_rec,
+            "value": 2.0 * g.M / (ms_rec / 1e3), "unit": UNIT,
+            "ms_per_step_unrecorded": ms_plain,
+            "cost_vs_unrecorded": ms_rec / ms_plain,
+            "blocks": f"{pairs} interleaved pairs of {B}-step calls (recorded / unrecorded)",
             "max_rel_energy_change": max(abs(E - em[0][0]) / abs(em[0][0]) for E, _ in em),
             "max_rel_mass_change": max(abs(m - em[0][1]) / abs(em[0][1]) for _, m in em),
             "note": "energy is the scheme's invariant (round-off drift); mass is not conserved "
