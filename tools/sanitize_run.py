@@ -38,12 +38,16 @@ def run(d, N, slabs=1, params=()):
 
 
 def main():
+    from paper_2502_09537_b200 import _lib
     run(3, 8)                                   # resident
-    run(3, 64)                                  # march, 1 slab
+    run(3, 64)                                  # march, 1 slab (MV4)
+    run(3, 64, 1, (("march_variant", 0),))      # march MV0
+    run(3, 64, 1, (("march_variant", 1),))      # march MV1
     run(3, 64, 4)                               # virtual slabs, fused halo stores
     run(3, 64, 2, (("mirror_halo", 0),))        # virtual slabs, copies
-    run(3, 64, 1, (("fused_step", 1),))         # fused step, 1 slab
-    run(3, 64, 2, (("fused_step", 1),))         # fused step, 2 slabs
+    if _lib.load().kgs_build_flags() & 1:       # experimental build only
+        run(3, 64, 1, (("fused_step", 1),))     # fused step, 1 slab
+        run(3, 64, 2, (("fused_step", 1),))     # fused step, 2 slabs
     run(2, 128)                                 # 2-D per-pass
     run(2, 128, 2)                              # 2-D slabs
     run(1, 8192)                                # 1-D per-pass (beyond resident size)
