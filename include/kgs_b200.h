@@ -251,7 +251,12 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
                    int march_planes, int march_variant);
 
 /* Named tuning knob (results never depend on it): "march_variant",
- * "march_planes", "march_sync" (planes between cluster barriers of the
+ * "march_planes", "march_wave_sync" (1, the default: a software grid
+ * barrier after every wave of work units of the marching kernel, so
+ * neighbouring columns march together and their shared halo rows / columns
+ * are re-read from L2 -- a bounded-spin performance heuristic, off for
+ * several slabs per GPU and inside kgs_integrate_host; 0: free-running),
+ * "march_sync" (planes between cluster barriers of the
  * clustered variants), "blocks_per_sm", "fused_step" (1: one fused march
  * per DP-AVF2 step -- K3 and K4 with ping-pong buffer sets, allocated on
  * first use; 3-D, rows % 16 == 0, slots % 32 == 0 -- bitwise equal but

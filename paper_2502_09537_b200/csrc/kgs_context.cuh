@@ -76,6 +76,8 @@ struct Slab {
   double* records = nullptr;                 // device [cap * NTERMS]
   int64_t rec_cap = 0;
   unsigned long long* bad = nullptr;
+  unsigned long long* wctr = nullptr;  // march wave-barrier arrivals (monotonic)
+  unsigned long long wbase = 0;        // arrivals of all earlier launches
   double* stage = nullptr;  // natural-layout staging planes
   int stage_planes = 0;
   cudaStream_t stream = nullptr;    // compute
@@ -123,6 +125,8 @@ struct kgs_ctx {
   int tune_variant = 4;  // march kernel variant (kgs_launch.cuh; MV4: 8 x 64 tiles, 2 rows per thread)
   int tune_promo_halo = 0, tune_promo_tile = 0;  // TMA L2 promotion (0 none .. 3 256B)
   int tune_sync = 4;     // march clusters: planes between cluster barriers
+  int tune_wsync = 1;    // march: software grid barrier after every wave of units
+  bool in_pipeline = false;  // kgs_integrate_host is issuing passes (wave barriers off)
   // deferred tail (KGS_STEP_DEFER_TAIL): the red adjoint of the last step is
   // pending and fuses with the next call's head when the coefficients match
   bool pending = false;

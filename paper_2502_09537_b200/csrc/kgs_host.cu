@@ -191,6 +191,7 @@ int kgs_destroy(kgs_ctx* ctx) {
     }
     if (s.records) cudaFree(s.records);
     if (s.bad) cudaFree(s.bad);
+    if (s.wctr) cudaFree(s.wctr);
     if (s.stage) cudaFree(s.stage);
     for (int c = 0; c < 2; ++c)
       if (s.alt[c]) cudaFree(s.alt[c]);
@@ -748,6 +749,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   if (!ctx || !name) return fail(ctx, KGS_EINVAL, "NULL argument");
   const std::string n(name);
   if (n == "march_sync") ctx->tune_sync = std::max(1, value);
+  else if (n == "march_wave_sync") ctx->tune_wsync = value;
   else if (n == "march_variant") {
     if (value >= kMarchVariantSlots || (value >= 0 && !kVarBuilt[value]))
       return fail(ctx, KGS_EINVAL, "march_variant %d not in this build (default build: 0, 1, "

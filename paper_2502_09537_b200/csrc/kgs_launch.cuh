@@ -240,7 +240,15 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   const int64_t cols = (int64_t)(g.ny / Var::TY) * (g.nk / Var::TK);
   const int nxr = g.xb - g.xa;
   MarchCfg mc;
+  // wave barriers (knob march_wave_sync, default on): one slab per device
+  // only (concurrent grids of other slabs or of the pipeline's transfers on
+  // the same GPU would keep CTAs of this one from being resident)
+  bool shared_dev = ctx->in_pipeline;
+  for (auto& t : ctx->slabs) shared_dev = shared_dev || (&t != &s && t.dev == s.dev);
+  mc.wsync = (ctx->tune_wsync && CL == 1 && !Var::PW && !shared_dev) ? 1 : 0;
   if (ctx->tune_xc > 0) mc.xc = std::min(ctx->tune_xc, nxr);
+  else if (mc.wsync)  // 256-plane units: drift reset every wave, few barriers
+    mc.xc = std::min(nxr, 256);
   else  // ~8 units per resident block for load balance, >= 8 planes per unit
     mc.xc = (int)std::max<int64_t>(std::min<int64_t>(nxr, 8),
                                    std::min<int64_t>(nxr, (int64_t)nxr * cols / (8 * G)));
@@ -248,6 +256,13 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   mc.sync = std::max(1, ctx->tune_sync);
   const int64_t grid = std::min<int64_t>(mc.nunits, G) / CL * CL;
   if (grid < 1) return KGS_OK;
+  // wave barriers: arrivals after waves 0 .. W-2
+  mc.wctr = s.wctr;
+  mc.wbase = s.wbase;
+  if (mc.wsync) {
+    const int64_t waves = (mc.nunits + grid - 1) / grid;
+    if (waves > 1) s.wbase += (unsigned long long)((waves - 1) * grid);
+  }
 
   if (CL > 1) {
     cudaLaunchConfig_t cfg = {};

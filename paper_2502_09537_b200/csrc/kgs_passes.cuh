@@ -351,6 +351,9 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
   }
   CK(cudaMalloc(&s.bad, sizeof(unsigned long long)));
   CK(cudaMemset(s.bad, 0xff, sizeof(unsigned long long)));
+  CK(cudaMalloc(&s.wctr, sizeof(unsigned long long)));
+  CK(cudaMemset(s.wctr, 0, sizeof(unsigned long long)));
+  s.wbase = 0;
 
   // staging: up to 256 MiB of natural-layout planes of one field
   const size_t nat_plane = (size_t)ctx->ny * ctx->nz * sizeof(double);

@@ -312,6 +312,12 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   for (int j = 0; j < J; ++j) shrink[j] = passes[j].shrink;
   const std::vector<PipeEvent> plan = pipeline_plan(N, C, shrink);
 
+  // the passes run next to the transfer streams' kernels: no wave barriers
+  struct PipeFlag {
+    kgs_ctx* c;
+    ~PipeFlag() { c->in_pipeline = false; }
+  } pipe_flag{ctx};
+  ctx->in_pipeline = true;
   auto launch_range = [&](const PipePass& P, int64_t xa, int64_t xb) -> int {
     if (xb <= xa) return KGS_OK;
     double* save = s.partials[P.col];
