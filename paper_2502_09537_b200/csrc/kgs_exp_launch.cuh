@@ -5,7 +5,7 @@
 #pragma once
 
 // fused step: red pieces of one buffer set (StepSmem layout)
-constexpr int kStepTY = 16, kStepTK = 32;
+constexpr int kStepTY = 8, kStepTK = 32;
 using StepS = StepSmem<kStepTY, kStepTK>;
 
 int make_step_maps(kgs_ctx* ctx, const Slab& s, double* red, StepMaps& m) {
@@ -97,16 +97,20 @@ void swap_sets(kgs_ctx* ctx) {
   }
 }
 
-template <bool DIAG, int K4OP2>
-int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int xb) {
+template <bool DIAG, int K4OP2, int FORM>
+int launch_step_form(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int xb) {
   constexpr int NT = kStepTY * kStepTK;
-  auto kern = step_pass<DIAG, K4OP2, kStepTY, kStepTK, 2>;
+  // FORM 1: step_pass (K4 one plane behind, 4 + 3 slots); FORM 2: step2_pass
+  // (K4 two planes behind, 5 + 4 slots, interleaved chains)
+  constexpr size_t kBytes = FORM == 1 ? StepS::bytes : Step2Smem<kStepTY, kStepTK, 5, 4>::bytes;
+  auto kern = FORM == 1 ? step_pass<DIAG, K4OP2, kStepTY, kStepTK, 2>
+                        : step2_pass<DIAG, K4OP2, kStepTY, kStepTK, 2>;
   static int occ_dev[kMaxDevices] = {};
   int& occ = occ_dev[current_device()];
   if (occ == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)StepS::bytes));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, StepS::bytes));
+                            (int)kBytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, kBytes));
     if (occ < 1) return fail(ctx, KGS_ECUDA, "fused step kernel does not fit on an SM");
   }
   StepGeom g{};
@@ -131,12 +135,18 @@ int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int
   const int64_t ncols = (int64_t)(ctx->ny / kStepTY) * (ctx->nk / kStepTK);
   g.nunits = (int64_t)((xb - xa + g.xc - 1) / g.xc) * ncols;
   const int64_t grid = std::min<int64_t>({g.nunits, (int64_t)occ * ctx->nsm, ctx->grid_cap});
-  kern<<<(unsigned)grid, NT, StepS::bytes, s.stream>>>(
+  kern<<<(unsigned)grid, NT, kBytes, s.stream>>>(
       s.smap[0], g, c, s.partials[1] + (int64_t)s.npart[1] * NTERMS, s.bad, step_no);
   ctx->launches++;
   if (DIAG) s.npart[1] += (int)grid;
   CK(cudaGetLastError());
   return KGS_OK;
+}
+
+template <bool DIAG, int K4OP2>
+int launch_step(kgs_ctx* ctx, Slab& s, const Coeffs& c, int step_no, int xa, int xb) {
+  return ctx->tune_fused == 2 ? launch_step_form<DIAG, K4OP2, 2>(ctx, s, c, step_no, xa, xb)
+                              : launch_step_form<DIAG, K4OP2, 1>(ctx, s, c, step_no, xa, xb);
 }
 
 

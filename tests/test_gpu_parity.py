@@ -369,7 +369,8 @@ def test_step_at_a_time_with_deferred_tail_is_bitwise(golden):
     (128, 7, 3, 1, 0), (256, 4, 4, 1, 0), (128, 1, 1, 1, 0), (64, 3, 1, 1, 0),
     (192, 3, 3, 1, 50), (128, 5, 5, 2, 0), (128, 4, 2, 4, 7), (64, 2, 1, 8, 0)])
 @needs_experimental
-def test_fused_step_matches_two_pass_and_oracle(N, steps, stride, slabs, planes):
+@pytest.mark.parametrize("form", [1, 2])
+def test_fused_step_matches_two_pass_and_oracle(N, steps, stride, slabs, planes, form):
     """One fused march per step (K3 on the tile + ring, K4 one plane behind,
     ping-pong buffer sets) gives the same bits as two colour passes, energy
     records equal to summation order, and (N <= 128) the same bits as the C
@@ -382,7 +383,7 @@ def test_fused_step_matches_two_pass_and_oracle(N, steps, stride, slabs, planes)
     args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
     ex = None if slabs == 1 else kgs.CudaExecutor((0,), slabs_per_device=slabs)
     outs = []
-    for fused in (0, 1):
+    for fused in (0, form):
         dev = (kgs.DeviceFieldState.from_host(s0, g, ex) if s0 is not None
                else kgs.DeviceFieldState.from_preset("ellipsoids3d", g, ex))
         dev.ctx.set_param("fused_step", fused)
