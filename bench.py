@@ -138,7 +138,12 @@ class Launch:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         ndev = torch.cuda.device_count()
-        if self.world > 1:
+        # torchrun with ONE rank and KGS_SELF_EXCHANGE=1: the rank exchanges
+        # its faces with itself over NCCL -- the multi-rank path on one GPU
+        self.selfx = (self.world == 1 and "WORLD_SIZE" in os.environ
+                      and os.environ.get("KGS_SELF_EXCHANGE") == "1")
+        self.dist = self.world > 1 or self.selfx
+        if self.dist:
             if self.local >= ndev:
                 raise SystemExit(f"bench.py: rank {self.rank} needs cuda:{self.local}, "
                                  f"only {ndev} devices visible")
@@ -148,7 +153,7 @@ class Launch:
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.devices = (self.local,)
             self.n_gpus = self.world
-            self.mode = "torchrun+nccl"
+            self.mode = "torchrun+nccl" + (" (1 rank, faces sent to itself)" if self.selfx else "")
         else:
             if gpus > ndev:
                 raise SystemExit(f"bench.py --gpus {gpus}: only {ndev} CUDA devices visible")
@@ -159,7 +164,7 @@ class Launch:
 
     def executor(self):
         import paper_2502_09537_b200 as kgs
-        if self.world > 1:
+        if self.dist:
             return kgs.DistributedExecutor(self.rank, self.world, self.local)
         return kgs.CudaExecutor(self.devices)
 

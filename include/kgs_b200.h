@@ -75,7 +75,12 @@ int kgs_create(int d, int64_t N, double a, double b, int nslabs,
  * context owns slab `rank` of `nranks` on `device`; face halos travel over
  * NCCL send/recv to ranks rank-1 / rank+1 (periodic).  `nccl_id` is the
  * 128-byte ncclUniqueId produced by kgs_nccl_unique_id on rank 0 and
- * broadcast by the caller.  nranks == 1 needs no NCCL (nccl_id may be NULL). */
+ * broadcast by the caller.  nranks == 1 needs no NCCL (nccl_id may be NULL).
+ * Test hook: nranks == 1 with a non-NULL nccl_id and KGS_SELF_EXCHANGE=1 in
+ * the environment makes the single slab exchange its faces with itself over
+ * NCCL instead of wrapping in the kernel -- the multi-rank code path (ghost
+ * planes, interior/boundary split, send/recv on the comm stream, event
+ * waits) run on one GPU. */
 int kgs_create_dist(int d, int64_t N, double a, double b, int rank, int nranks,
                     int device, const void* nccl_id, kgs_ctx** out);
 
@@ -165,14 +170,18 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
                        int64_t record_stride, double* terms0, double* terms_out,
                        int64_t* first_bad_step, int flags);
 
-/* The schedule kgs_integrate_host executes for N planes, chunks of C planes
- * and nsteps steps, as events (kind, index, a, b) written to out[4 * i ..]
- * (at most `cap` events): kind 0 = chunk `index` (planes [a, b)) arrived,
- * 1 = pass `index` over planes [a, b) (passes: 0 black energy terms, 1 red
- * energy terms, 2 head, then K3/K4 per step), 2 = block `index` (planes
- * [a, b)) final and copied back.  Pure host logic (no device); returns the
- * number of events, -1 on bad arguments. */
-int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap);
+/* The schedule kgs_integrate_host executes for N (local) planes, chunks of C
+ * planes and nsteps steps, as events (kind, index, a, b) written to
+ * out[4 * i ..] (at most `cap` events): kind 0 = chunk `index` (planes
+ * [a, b)) arrived, 1 = pass `index` over planes [a, b) (passes: 0 black
+ * energy terms, 1 red energy terms, 2 head, then K3/K4 per step), 2 = block
+ * `index` (planes [a, b)) final and copied back, 3 (split = 1: several slabs
+ * or ranks, every one running this plan on its own planes) = exchange the
+ * faces pass `index` wrote (-1: both colours of the arrived state).  Pure
+ * host logic (no device); returns the number of events, -1 on bad
+ * arguments. */
+int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int split, int64_t* out,
+                          int64_t cap);
 
 /* The pass program kgs_step_dpavf2 executes on every slab / rank of `nx`
  * local planes (split = 1: several slabs or ranks, faces exchanged; 0: one

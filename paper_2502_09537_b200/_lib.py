@@ -92,7 +92,7 @@ def load() -> ctypes.CDLL:
         "kgs_integrate_host": (ctypes.c_int, [_P, _DP, _DP, _DP, _DP, ctypes.POINTER(KgsCoeffs),
                                               _I64, _I64, _I64, _DP, _DP,
                                               ctypes.POINTER(_I64), ctypes.c_int]),
-        "kgs_pipeline_plan": (_I64, [_I64, _I64, _I64, ctypes.POINTER(_I64), _I64]),
+        "kgs_pipeline_plan": (_I64, [_I64, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64), _I64]),
         "kgs_restore_backup": (ctypes.c_int, [_P]),
         "kgs_step_program": (_I64, [_I64, ctypes.c_int, _I64, _I64, _I64, ctypes.c_int,
                                     ctypes.POINTER(_I64), _I64]),

@@ -89,6 +89,7 @@ struct Slab {
   cudaEvent_t ev_face[2] = {nullptr, nullptr};  // boundary planes of pass k written (k & 1)
   // pipelined host integration (kgs_integrate_host)
   cudaStream_t dstream = nullptr;   // downloads
+  cudaStream_t ustream = nullptr;   // uploads (off the comm stream: exchanges must not queue behind them)
   double* pipe_up = nullptr;        // natural-layout staging, one chunk of 4 fields
   double* pipe_dn = nullptr;
   int64_t pipe_stage = 0;           // doubles per staging buffer
@@ -113,6 +114,9 @@ struct kgs_ctx {
   std::vector<Slab> slabs;
   bool dist = false;
   int rank = 0, nranks = 1;
+  // a 1-rank dist context that exchanges its faces with itself over NCCL
+  // (KGS_SELF_EXCHANGE=1 test hook, kgs_create_dist): the multi-rank path on one GPU
+  bool self_xch = false;
   ncclComm_t comm = nullptr;
   std::string err = "no error";
   std::atomic<int64_t> launches{0};   // our kernel launches (the pipeline uploader thread adds too)
@@ -156,6 +160,12 @@ struct kgs_ctx {
   int64_t pass_count = 0;
   double pass_ms = 0.0;
 };
+
+// Faces travel between slabs (several slabs, or ranks -- possibly one
+// exchanging with itself); otherwise the single slab wraps in the kernel.
+bool needs_exchange(const kgs_ctx* ctx) {
+  return ctx->dist ? (ctx->nranks > 1 || ctx->self_xch) : ctx->slabs.size() > 1;
+}
 
 namespace {
 
@@ -211,7 +221,7 @@ PassGeom make_geom(const kgs_ctx* ctx, const Slab& s, int col, int xa, int xb) {
   g.xa = xa;
   g.xb = xb;
   g.x0 = s.x0;
-  g.wrap = (ctx->slabs.size() == 1 && !(ctx->dist && ctx->nranks > 1)) ? 1 : 0;
+  g.wrap = needs_exchange(ctx) ? 0 : 1;
   // 3-D: tk slots x ty rows (rows y+-1 shared through L1 inside the tile);
   // otherwise one row segment of up to 256 slots.
   int tk = std::min(kThreads, pow2ceil(ctx->nk));

@@ -43,7 +43,7 @@ using namespace kgs;
 // =========================================================================
 extern "C" {
 
-int kgs_abi_version(void) { return 101; }
+int kgs_abi_version(void) { return 102; }
 
 int kgs_device_count(void) {
   int n = 0;
@@ -143,6 +143,10 @@ int kgs_create_dist(int d, int64_t N, double a, double b, int rank, int nranks,
   ctx->dist = true;
   ctx->rank = rank;
   ctx->nranks = nranks;
+  if (nranks == 1 && nccl_id) {
+    const char* e = std::getenv("KGS_SELF_EXCHANGE");
+    ctx->self_xch = e && e[0] == '1';
+  }
   int r = init_geometry(ctx, d, N, a, b);
   if (!r && (nranks < 1 || rank < 0 || rank >= nranks)) r = fail(ctx, KGS_EINVAL, "bad rank %d of %d", rank, nranks);
   if (!r && nranks > 1 && d == 1) r = fail(ctx, KGS_EINVAL, "1-D grids cannot be split into slabs");
@@ -157,7 +161,7 @@ int kgs_create_dist(int d, int64_t N, double a, double b, int rank, int nranks,
     s.x0 = (int64_t)rank * s.nx;
     r = alloc_slab(ctx, s);
   }
-  if (!r && nranks > 1) {
+  if (!r && (nranks > 1 || ctx->self_xch)) {
     std::string err;
     if (!nccl_id) r = fail(ctx, KGS_EINVAL, "nccl_id is NULL");
     else if (!load_nccl(err)) r = fail(ctx, KGS_ENCCL, "%s", err.c_str());
@@ -204,10 +208,12 @@ int kgs_destroy(kgs_ctx* ctx) {
     for (int i = 0; i < 2; ++i)
       if (s.ev_face[i]) cudaEventDestroy(s.ev_face[i]);
     if (s.dstream) cudaStreamSynchronize(s.dstream);
+    if (s.ustream) cudaStreamSynchronize(s.ustream);
     for (auto e : s.pipe_ev) cudaEventDestroy(e);
     for (auto e : s.hslot_ev) cudaEventDestroy(e);
     if (s.hslot) cudaFreeHost(s.hslot);
     if (s.dstream) cudaStreamDestroy(s.dstream);
+    if (s.ustream) cudaStreamDestroy(s.ustream);
     if (s.pipe_up) cudaFree(s.pipe_up);
     if (s.pipe_dn) cudaFree(s.pipe_dn);
     if (s.pipe_part) cudaFree(s.pipe_part);
@@ -522,9 +528,12 @@ int64_t kgs_step_program(int64_t nx, int split, int64_t nsteps, int64_t step_off
   return n;
 }
 
-int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int64_t* out, int64_t cap) {
+int64_t kgs_pipeline_plan(int64_t N, int64_t C, int64_t nsteps, int split, int64_t* out,
+                          int64_t cap) {
   if (N < 1 || C < 1 || nsteps < 0 || cap < 0 || (cap > 0 && !out)) return -1;
-  const std::vector<PipeEvent> plan = pipeline_plan(N, C, pipeline_shrinks(nsteps));
+  const std::vector<char> writes = pipeline_writes(nsteps);
+  const std::vector<PipeEvent> plan =
+      pipeline_plan(N, C, pipeline_shrinks(nsteps), split ? &writes : nullptr);
   const int64_t n = (int64_t)plan.size();
   for (int64_t i = 0; i < std::min(n, cap); ++i) {
     out[4 * i] = plan[i].kind;
@@ -579,18 +588,28 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
     return kgs_download(ctx, P, Q, U, V);
   }
   if (r) return r;
-  Slab& s = ctx->slabs[0];
-  std::vector<double> rec((size_t)(nrec + 1) * NTERMS);
-  CK(cudaMemcpy(rec.data(), s.records, rec.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> rec((size_t)(nrec + 1) * NTERMS), tmp(rec.size());
+  for (auto& s : ctx->slabs) {   // slab order: deterministic host sum (as kgs_step_dpavf2)
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemcpy(tmp.data(), s.records, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < rec.size(); ++q) rec[q] += tmp[q];
+  }
   std::copy(rec.begin(), rec.begin() + NTERMS, terms0);
   if (nrec > 0) std::copy(rec.begin() + NTERMS, rec.end(), terms_out);
   if (bad != ULLONG_MAX) {
     // restore the initial state (device copy) and replay exactly to the bad step
     // (on the slab stream: a device-to-device cudaMemcpy would not order
-    // itself before the replay's kernels on this non-blocking stream)
-    for (int cc = 0; cc < 2; ++cc)
-      CK(cudaMemcpyAsync(s.buf[cc], s.alt[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
-                         cudaMemcpyDeviceToDevice, s.stream));
+    // itself before the replay's kernels on this non-blocking stream); the
+    // copy holds no ghost planes, so several slabs exchange their faces first
+    for (auto& s : ctx->slabs) {
+      CK(cudaSetDevice(s.dev));
+      for (int cc = 0; cc < 2; ++cc)
+        CK(cudaMemcpyAsync(s.buf[cc], s.alt[cc], (size_t)(s.nx + 2) * ctx->ps * 8,
+                           cudaMemcpyDeviceToDevice, s.stream));
+    }
+    r = exchange(ctx, 0);
+    if (!r) r = exchange(ctx, 1);
+    if (r) return r;
     int64_t fb2 = 0;
     r = KGS_OK;
     if ((int64_t)bad > step_offset)

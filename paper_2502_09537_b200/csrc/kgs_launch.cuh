@@ -295,7 +295,7 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
 constexpr size_t kResidentMaxBytes = 200 * 1024;
 
 bool resident_eligible(const kgs_ctx* ctx) {
-  if (!ctx->tune_resident || ctx->slabs.size() != 1 || (ctx->dist && ctx->nranks > 1))
+  if (!ctx->tune_resident || ctx->slabs.size() != 1 || needs_exchange(ctx))
     return false;
   const Slab& s = ctx->slabs[0];
   return (size_t)s.nx * ctx->ps * 2 * sizeof(double) <= kResidentMaxBytes;
@@ -336,7 +336,6 @@ int launch_resident(kgs_ctx* ctx, const Coeffs& c, int64_t nsteps, int64_t step_
   }
 }
 
-bool needs_exchange(const kgs_ctx* ctx);
 int exchange(kgs_ctx* ctx, int col);
 int launch_pass(kgs_ctx* ctx, Slab& s, int col, int op1, int op2, bool diag,
                 bool check, const Coeffs& c, int step_no, int xa, int xb,

@@ -7,10 +7,6 @@ namespace {
 // ---- halo exchange of colour `col` faces (P, Q, U of planes 0 and nx-1) --
 // The three fields of a plane are contiguous ([P|Q|U|V] per plane), so a
 // face is ONE contiguous run of 3*pp doubles.
-bool needs_exchange(const kgs_ctx* ctx) {
-  return ctx->dist ? ctx->nranks > 1 : ctx->slabs.size() > 1;
-}
-
 // Start the exchange of colour `col` faces (P, Q, U of planes 0 and nx-1)
 // on each slab's comm stream, after the boundary planes of the pass that
 // wrote them (ev_bnd); completion is ev_xch, which the next pass waits for

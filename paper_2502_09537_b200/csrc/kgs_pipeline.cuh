@@ -56,20 +56,44 @@ constexpr int kPipeFallback = 1;   // not eligible / no memory: use the plain pa
 
 // The pipeline as a list of events, in the order they are issued on the
 // compute stream: ARRIVE (wait for chunk m = planes [a, b)), PASS (pass j
-// over planes [a, b)), FINAL (planes [a, b) are final: copy them back).
+// over planes [a, b)), FINAL (planes [a, b) are final: copy them back),
+// XCH (several slabs / ranks: exchange the faces pass j wrote; j = -1: both
+// colours' faces of the arrived state).
 // Pure host logic (kgs_pipeline_plan exports it for the CPU tests).
-enum PipeKind : int { PIPE_ARRIVE = 0, PIPE_PASS = 1, PIPE_FINAL = 2 };
+//
+// Several slabs (`writes` given): every slab runs the same plan on its own
+// planes, so a slab's local plane -1 (unwrapped) is its lower neighbour's
+// plane nx-1, which that neighbour covers at the same point of the same plan
+// -- the done regions are intervals around every slab boundary, and a pass
+// reads its ghost planes only in launches covering plane 0 or nx-1.  So a
+// writing pass's faces are exchanged as soon as it has covered both
+// boundary planes (before any launch of its successor can reach them, which
+// needs exactly that coverage), and a launch covering a boundary plane
+// waits for the pending exchange.  The arrived state's faces are exchanged
+// once both boundary blocks are in (the first two chunks, folded order).
+enum PipeKind : int { PIPE_ARRIVE = 0, PIPE_PASS = 1, PIPE_FINAL = 2, PIPE_XCH = 3 };
 struct PipeEvent {
   int kind, pass;
   int64_t a, b;
 };
 
-std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int>& shrink) {
+std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int>& shrink,
+                                     const std::vector<char>* writes = nullptr) {
   std::vector<PipeEvent> ev;
   const int64_t nb = (N + C - 1) / C;
   const int J = (int)shrink.size();
   std::vector<int64_t> lo(J, 0), hi(J, 0);   // done regions, unwrapped: empty or lo < hi
-  std::vector<char> dl(nb, 0);
+  std::vector<char> dl(nb, 0), xch(J, 0);
+  // unwrapped region of pass j contains plane x (or the whole ring)
+  auto covers = [&](int j, int64_t x) {
+    return hi[j] - lo[j] >= N || (lo[j] <= x && x < hi[j]) || (lo[j] <= x - N && x - N < hi[j]);
+  };
+  auto exchange_after = [&](int j) {   // pass j's faces, once both boundary planes are done
+    if (writes && (*writes)[j] && !xch[j] && covers(j, 0) && covers(j, N - 1)) {
+      xch[j] = 1;
+      ev.push_back({PIPE_XCH, j, 0, 0});
+    }
+  };
   auto pass = [&](int j, int64_t a, int64_t b) {
     if (b > a) ev.push_back({PIPE_PASS, j, a, b});
   };
@@ -110,6 +134,7 @@ std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int
           }
         }
       }
+      exchange_after(j);
       plo = lo[j];
       phi = hi[j];
     }
@@ -132,6 +157,8 @@ std::vector<PipeEvent> pipeline_plan(int64_t N, int64_t C, const std::vector<int
     ev.push_back({PIPE_ARRIVE, (int)m, x0, x1});
     if (m % 2 == 0) ahi = x1; else alo = x0 - N;
     if (m == nb - 1) { alo = 0; ahi = N; }       // the whole ring has arrived
+    if (writes && m == std::min<int64_t>(1, nb - 1))   // blocks 0 and nb-1 are in
+      ev.push_back({PIPE_XCH, -1, 0, 0});
     round(alo, ahi);
   }
   for (int guard = 0; !full(J - 1) && guard < 4 * (int)nb + J + 4; ++guard) round(0, N);
@@ -143,6 +170,13 @@ std::vector<int> pipeline_shrinks(int64_t nsteps) {
   std::vector<int> sh = {0, 1, 0};
   for (int64_t i = 0; i < 2 * nsteps; ++i) sh.push_back(1);
   return sh;
+}
+
+std::vector<char> pipeline_writes(int64_t nsteps) {
+  // the energy passes only read; the head and every K3/K4 write their colour
+  std::vector<char> w = {0, 0, 1};
+  for (int64_t i = 0; i < 2 * nsteps; ++i) w.push_back(1);
+  return w;
 }
 
 // ---- pageable host arrays: page-locked bounce slots ---------------------
@@ -240,57 +274,74 @@ int ensure_host_slots(kgs_ctx* ctx, Slab& s, int64_t slot) {
 int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, int64_t nsteps,
                         int64_t step_offset, int64_t record_stride, int64_t nrec,
                         unsigned long long* bad_out) {
-  if (!ctx->tune_pipe || ctx->slabs.size() != 1 || ctx->dist || ctx->d != 3)
-    return kPipeFallback;
-  Slab& s = ctx->slabs[0];
-  const int64_t N = s.nx;
+  if (!ctx->tune_pipe || ctx->d != 3) return kPipeFallback;
+  const int ns = (int)ctx->slabs.size();
+  // several slabs / ranks: every slab runs the same plan on its own planes,
+  // with face exchanges between the passes (pipeline_plan)
+  const bool split = needs_exchange(ctx);
+  const int64_t N = ctx->slabs[0].nx;   // planes per slab
+  for (const Slab& s : ctx->slabs)
+    if (s.nx != N) return kPipeFallback;
   // chunk planes; a layout-transform launch covers < 2^31 point pairs (decode_point)
   const int64_t C = std::max<int64_t>(1, std::min<int64_t>(ctx->tune_pipe_chunk,
                                                            ((1ll << 31) - 1) / ((int64_t)ctx->ny * ctx->nk)));
   const int64_t nb = (N + C - 1) / C;
   if (nb < 4) return kPipeFallback;
   const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
-  CK(cudaSetDevice(s.dev));
+  // pageable arrays (the reference's numpy FieldState): staged through
+  // page-locked slots by host threads -- one slab's pipeline; several slabs
+  // take the plain path for them.  Page-locked arrays (FieldState.pinned) go direct.
+  bool staged = false;
+  if (ctx->tune_stage)
+    for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
+  if (staged && ns > 1) return kPipeFallback;
   if (ensure_alt(ctx)) return kPipeFallback;
   const int64_t stage = 4 * C * nat_plane;
-  if (s.pipe_stage < stage) {
-    if (s.pipe_up) CK(cudaFree(s.pipe_up));
-    if (s.pipe_dn) CK(cudaFree(s.pipe_dn));
-    s.pipe_up = s.pipe_dn = nullptr;
-    s.pipe_stage = 0;
-    if (cudaMalloc(&s.pipe_up, stage * 8) != cudaSuccess ||
-        cudaMalloc(&s.pipe_dn, stage * 8) != cudaSuccess) {
-      cudaGetLastError();
-      if (s.pipe_up) cudaFree(s.pipe_up);
-      s.pipe_up = nullptr;
-      return kPipeFallback;
-    }
-    s.pipe_stage = stage;
-  }
   const int64_t maxl = nb + 4;                                 // launches per pass
   const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
   const int64_t need = (nrec + 1) * 2 * region;
-  if (s.pipe_part_cap < need) {
-    if (need > (int64_t)1 << 27) return kPipeFallback;         // > 1 GiB of partials
-    if (s.pipe_part) CK(cudaFree(s.pipe_part));
-    s.pipe_part = nullptr;
-    s.pipe_part_cap = 0;
-    if (cudaMalloc(&s.pipe_part, need * 8) != cudaSuccess) {
-      cudaGetLastError();
-      return kPipeFallback;
+  if (need > (int64_t)1 << 27) return kPipeFallback;           // > 1 GiB of partials per slab
+  for (Slab& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    if (s.pipe_stage < stage) {
+      if (s.pipe_up) CK(cudaFree(s.pipe_up));
+      if (s.pipe_dn) CK(cudaFree(s.pipe_dn));
+      s.pipe_up = s.pipe_dn = nullptr;
+      s.pipe_stage = 0;
+      if (cudaMalloc(&s.pipe_up, stage * 8) != cudaSuccess ||
+          cudaMalloc(&s.pipe_dn, stage * 8) != cudaSuccess) {
+        cudaGetLastError();
+        if (s.pipe_up) cudaFree(s.pipe_up);
+        s.pipe_up = nullptr;
+        return kPipeFallback;
+      }
+      s.pipe_stage = stage;
     }
-    s.pipe_part_cap = need;
-  }
-  if (!s.dstream) CK(cudaStreamCreateWithFlags(&s.dstream, cudaStreamNonBlocking));
-  while ((int64_t)s.pipe_ev.size() < 2 * nb) {
-    cudaEvent_t e;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    s.pipe_ev.push_back(e);
+    if (s.pipe_part_cap < need) {
+      if (s.pipe_part) CK(cudaFree(s.pipe_part));
+      s.pipe_part = nullptr;
+      s.pipe_part_cap = 0;
+      if (cudaMalloc(&s.pipe_part, need * 8) != cudaSuccess) {
+        cudaGetLastError();
+        return kPipeFallback;
+      }
+      s.pipe_part_cap = need;
+    }
+    if (!s.dstream) CK(cudaStreamCreateWithFlags(&s.dstream, cudaStreamNonBlocking));
+    if (!s.ustream) CK(cudaStreamCreateWithFlags(&s.ustream, cudaStreamNonBlocking));
+    while ((int64_t)s.pipe_ev.size() < 2 * nb) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s.pipe_ev.push_back(e);
+    }
   }
   int r = ensure_records(ctx, nrec + 1);
   if (!r) r = reset_bad(ctx);
   if (r) return r;
   ctx->pending = false;   // the whole state is replaced
+  // the ghost planes are filled by this call's own exchanges
+  ctx->mirrored[0] = ctx->mirrored[1] = false;
+  for (Slab& s : ctx->slabs) s.xch_pending = false;
 
   // the passes of the call: initial energy (black self, red edges + self),
   // head, then K3(n), K4(n) per step (K4 of the last step = the tail)
@@ -307,10 +358,12 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     passes.push_back({1, OP_ADJ, i < nsteps ? OP_BASE : OP_NONE, rec, true, (int)n, rid, 1});
   }
   const int J = (int)passes.size();
-  std::vector<int64_t> roff((size_t)(nrec + 1) * 2, 0);
   std::vector<int> shrink(J);
   for (int j = 0; j < J; ++j) shrink[j] = passes[j].shrink;
-  const std::vector<PipeEvent> plan = pipeline_plan(N, C, shrink);
+  const std::vector<char> writes = pipeline_writes(nsteps);
+  const std::vector<PipeEvent> plan = pipeline_plan(N, C, shrink, split ? &writes : nullptr);
+  // partials written so far per (slab, record, colour)
+  std::vector<std::vector<int64_t>> roff(ns, std::vector<int64_t>((size_t)(nrec + 1) * 2, 0));
 
   // the passes run next to the transfer streams' kernels: no wave barriers
   struct PipeFlag {
@@ -318,32 +371,34 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     ~PipeFlag() { c->in_pipeline = false; }
   } pipe_flag{ctx};
   ctx->in_pipeline = true;
-  auto launch_range = [&](const PipePass& P, int64_t xa, int64_t xb) -> int {
+  auto launch_range = [&](int si, const PipePass& P, int64_t xa, int64_t xb) -> int {
     if (xb <= xa) return KGS_OK;
+    Slab& s = ctx->slabs[si];
+    CK(cudaSetDevice(s.dev));
+    if (s.xch_pending && (xa == 0 || xb == s.nx)) {   // reads the ghost planes
+      CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+      s.xch_pending = false;
+    }
     double* save = s.partials[P.col];
     const int64_t ri = P.diag ? (int64_t)P.rec * 2 + P.col : 0;
     if (P.diag) {
       s.partials[P.col] = s.pipe_part + ri * region;
-      s.npart[P.col] = (int)roff[ri];
+      s.npart[P.col] = (int)roff[si][ri];
     }
     int rr = launch_pass(ctx, s, P.col, P.op1, P.op2, P.diag, P.check, c, P.step_no, (int)xa,
                          (int)xb);
     if (P.diag) {
-      roff[ri] = s.npart[P.col];
+      roff[si][ri] = s.npart[P.col];
       s.partials[P.col] = save;
     }
     return rr;
   };
 
-  // pageable arrays (the reference's numpy FieldState): stage through
-  // page-locked slots; page-locked arrays (FieldState.pinned) go direct
-  bool staged = false;
-  if (ctx->tune_stage)
-    for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
-  if (staged && ensure_host_slots(ctx, s, stage) != KGS_OK) staged = false;
+  Slab& s0 = ctx->slabs[0];
+  if (staged && ensure_host_slots(ctx, s0, stage) != KGS_OK) staged = false;
   // host threads per direction (uploads and downloads copy concurrently)
   const int cp_threads = std::max(1, std::min(8, ((int)std::thread::hardware_concurrency() - 2) / 2));
-  auto up_slot = [&](int64_t m) { return s.hslot + (m % kUpSlots) * stage; };
+  auto up_slot = [&](int64_t m) { return s0.hslot + (m % kUpSlots) * stage; };
   // KGS_PIPE_DEBUG=1: host-side time breakdown of a staged call on stderr
   static const bool dbg = std::getenv("KGS_PIPE_DEBUG") != nullptr;
   using clk = std::chrono::steady_clock;
@@ -352,13 +407,24 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   };
   const clk::time_point t_call = clk::now();
   double up_wait = 0, up_copy = 0, dn_wait = 0, dn_copy = 0, main_wait_up = 0, main_wait_dn = 0;
-  auto dn_slot = [&](int64_t j) { return s.hslot + (kUpSlots + j % kDnSlots) * stage; };
+  auto dn_slot = [&](int64_t j) { return s0.hslot + (kUpSlots + j % kDnSlots) * stage; };
 
-  CK(cudaEventRecord(s.ev_t0, s.cstream));
-  // uploads (folded block order) on the comm stream: H2D, split, backup copy
-  auto upload_chunk = [&](const PipeEvent& e) -> int {
+  CK(cudaSetDevice(s0.dev));
+  CK(cudaEventRecord(s0.ev_t0, s0.stream));
+  for (Slab& s : ctx->slabs) {   // uploads start after the call does
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamWaitEvent(s.ustream, s0.ev_t0, 0));
+  }
+  // uploads (folded block order) on the upload stream: H2D, split, backup
+  // copy.  The host arrays hold this context's planes (kgs_upload's
+  // convention: the whole grid, or a rank's slab), slab s from s.x0 - hx0 on.
+  int64_t hx0 = 0;
+  kgs_local_range(ctx, &hx0, nullptr, nullptr);
+  auto upload_chunk = [&](Slab& s, const PipeEvent& e) -> int {
     const int64_t m = e.pass, x0 = e.a, x1 = e.b, nxc = x1 - x0;
+    const int64_t gx = s.x0 - hx0 + x0;
     const size_t bytes = (size_t)nxc * nat_plane * 8;
+    CK(cudaSetDevice(s.dev));
     if (staged) {
       cudaEvent_t done = s.hslot_ev[m % kUpSlots];
       const clk::time_point t0 = clk::now();
@@ -366,18 +432,18 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       const clk::time_point t1 = clk::now();
       double* sl = up_slot(m);
       for (int f = 0; f < 4; ++f)
-        par_copy((char*)(sl + f * C * nat_plane), (const char*)(host[f] + x0 * nat_plane), bytes,
+        par_copy((char*)(sl + f * C * nat_plane), (const char*)(host[f] + gx * nat_plane), bytes,
                  cp_threads);
       up_wait += secs(t0, t1);
       up_copy += secs(t1, clk::now());
       for (int f = 0; f < 4; ++f)
         CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, sl + f * C * nat_plane, bytes,
-                           cudaMemcpyHostToDevice, s.cstream));
-      CK(cudaEventRecord(done, s.cstream));
+                           cudaMemcpyHostToDevice, s.ustream));
+      CK(cudaEventRecord(done, s.ustream));
     } else {
       for (int f = 0; f < 4; ++f)
-        CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + x0 * nat_plane, bytes,
-                           cudaMemcpyHostToDevice, s.cstream));
+        CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + gx * nat_plane, bytes,
+                           cudaMemcpyHostToDevice, s.ustream));
     }
     const int64_t cnt = nxc * ctx->ny * ctx->nk;
     const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
@@ -385,15 +451,15 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       PassGeom g = make_geom(ctx, s, 1, 0, s.nx);   // own = red, oth = black
       g.own += f * ctx->pp;
       g.oth += f * ctx->pp;
-      split_field<<<blocks, 256, 0, s.cstream>>>(s.pipe_up + f * C * nat_plane, g, (int)nxc,
-                                                  (int)x0);
+      split_field<<<blocks, 256, 0, s.ustream>>>(s.pipe_up + f * C * nat_plane, g, (int)nxc,
+                                                   (int)x0);
       ctx->launches++;
     }
     CK(cudaGetLastError());
     for (int cc = 0; cc < 2; ++cc)
       CK(cudaMemcpyAsync(s.alt0[cc] + x0 * ctx->ps, s.plane0[cc] + x0 * ctx->ps,
-                         (size_t)nxc * ctx->ps * 8, cudaMemcpyDeviceToDevice, s.cstream));
-    CK(cudaEventRecord(s.pipe_ev[m], s.cstream));
+                         (size_t)nxc * ctx->ps * 8, cudaMemcpyDeviceToDevice, s.ustream));
+    CK(cudaEventRecord(s.pipe_ev[m], s.ustream));
     return KGS_OK;
   };
 
@@ -412,10 +478,10 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   std::thread uploader, downloader;
   if (staged) {
     uploader = std::thread([&] {
-      cudaSetDevice(s.dev);
+      cudaSetDevice(s0.dev);
       for (const PipeEvent& e : plan) {
         if (e.kind != PIPE_ARRIVE) continue;
-        const int rc = upload_chunk(e);
+        const int rc = upload_chunk(s0, e);
         {
           std::lock_guard<std::mutex> lk(mu);
           if (rc && !err) err = rc;
@@ -426,7 +492,7 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       }
     });
     downloader = std::thread([&] {
-      cudaSetDevice(s.dev);
+      cudaSetDevice(s0.dev);
       for (;;) {
         DlJob jb;
         {
@@ -436,14 +502,15 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
           jb = dl_queue[dl_next++];
         }
         const clk::time_point t0 = clk::now();
-        int rc = cudaEventSynchronize(s.hslot_ev[kUpSlots + jb.j % kDnSlots]) == cudaSuccess
+        int rc = cudaEventSynchronize(s0.hslot_ev[kUpSlots + jb.j % kDnSlots]) == cudaSuccess
                      ? KGS_OK : fail(ctx, KGS_ECUDA, "download slot event failed");
         const clk::time_point t1 = clk::now();
         if (!rc) {
           const double* sl = dn_slot(jb.j);
           for (int f = 0; f < 4; ++f)
-            par_copy((char*)(host[f] + jb.b0 * nat_plane), (const char*)(sl + f * C * nat_plane),
-                     (size_t)jb.nxc * nat_plane * 8, cp_threads);
+            par_copy((char*)(host[f] + (s0.x0 - hx0 + jb.b0) * nat_plane),
+                     (const char*)(sl + f * C * nat_plane), (size_t)jb.nxc * nat_plane * 8,
+                     cp_threads);
         }
         dn_wait += secs(t0, t1);
         dn_copy += secs(t1, clk::now());
@@ -458,7 +525,8 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   } else {
     for (const PipeEvent& e : plan) {
       if (e.kind != PIPE_ARRIVE) continue;
-      if (int rc = upload_chunk(e)) return rc;
+      for (Slab& s : ctx->slabs)
+        if (int rc = upload_chunk(s, e)) return rc;
     }
   }
   // join the helper threads on every exit path
@@ -479,7 +547,8 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     }
   } joiner{uploader, downloader, mu, cv, dl_close};
 
-  // the wavefront on the compute stream; downloads behind it
+  // the wavefront on the compute streams (every slab in step); face
+  // exchanges between the passes; downloads behind it
   int64_t ndl = 0;
   for (const PipeEvent& e : plan) {
     if (r) break;
@@ -491,15 +560,22 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
         main_wait_up += secs(t0, clk::now());
         if (err) return err;
       }
-      CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[e.pass], 0));
+      for (Slab& s : ctx->slabs) {
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamWaitEvent(s.stream, s.pipe_ev[e.pass], 0));
+      }
+    } else if (e.kind == PIPE_XCH) {
+      if (e.pass < 0) {
+        r = exchange(ctx, 0);
+        if (!r) r = exchange(ctx, 1);
+      } else {
+        r = exchange(ctx, passes[e.pass].col);
+      }
     } else if (e.kind == PIPE_PASS) {
-      r = launch_range(passes[e.pass], e.a, e.b);
+      for (int si = 0; si < ns && !r; ++si) r = launch_range(si, passes[e.pass], e.a, e.b);
     } else {
       const int64_t k = e.pass, b0 = e.a, nxc = e.b - e.a;
       const int64_t j = ndl++;
-      cudaEvent_t ev = s.pipe_ev[nb + k];
-      CK(cudaEventRecord(ev, s.stream));
-      CK(cudaStreamWaitEvent(s.dstream, ev, 0));
       const int64_t cnt = nxc * ctx->ny * ctx->nk;
       const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
       if (staged) {   // the download slot must have been emptied by the downloader
@@ -509,20 +585,27 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
         main_wait_dn += secs(t0, clk::now());
         if (err) return err;
       }
-      for (int f = 0; f < 4; ++f) {
-        PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
-        g.own += f * ctx->pp;
-        g.oth += f * ctx->pp;
-        merge_field<<<blocks, 256, 0, s.dstream>>>(s.pipe_dn + f * C * nat_plane, g, (int)nxc,
-                                                    (int)b0);
-        ctx->launches++;
-        double* to = staged ? dn_slot(j) + f * C * nat_plane : host[f] + b0 * nat_plane;
-        CK(cudaMemcpyAsync(to, s.pipe_dn + f * C * nat_plane, (size_t)nxc * nat_plane * 8,
-                           cudaMemcpyDeviceToHost, s.dstream));
+      for (Slab& s : ctx->slabs) {
+        CK(cudaSetDevice(s.dev));
+        cudaEvent_t ev = s.pipe_ev[nb + k];
+        CK(cudaEventRecord(ev, s.stream));
+        CK(cudaStreamWaitEvent(s.dstream, ev, 0));
+        for (int f = 0; f < 4; ++f) {
+          PassGeom g = make_geom(ctx, s, 1, 0, s.nx);
+          g.own += f * ctx->pp;
+          g.oth += f * ctx->pp;
+          merge_field<<<blocks, 256, 0, s.dstream>>>(s.pipe_dn + f * C * nat_plane, g, (int)nxc,
+                                                      (int)b0);
+          ctx->launches++;
+          double* to = staged ? dn_slot(j) + f * C * nat_plane
+                              : host[f] + (s.x0 - hx0 + b0) * nat_plane;
+          CK(cudaMemcpyAsync(to, s.pipe_dn + f * C * nat_plane, (size_t)nxc * nat_plane * 8,
+                             cudaMemcpyDeviceToHost, s.dstream));
+        }
+        CK(cudaGetLastError());
       }
-      CK(cudaGetLastError());
       if (staged) {
-        CK(cudaEventRecord(s.hslot_ev[kUpSlots + j % kDnSlots], s.dstream));
+        CK(cudaEventRecord(s0.hslot_ev[kUpSlots + j % kDnSlots], s0.dstream));
         {
           std::lock_guard<std::mutex> lk(mu);
           dl_queue.push_back({b0, nxc, j});
@@ -545,21 +628,34 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   if (r) return r;
   if (ndl != nb) return fail(ctx, KGS_ECUDA, "pipeline copied back %lld of %lld blocks",
                              (long long)ndl, (long long)nb);
-  for (int64_t q = 0; q <= nrec; ++q) {
-    finalize_terms<<<1, kThreads, 0, s.stream>>>(
-        s.pipe_part + (q * 2 + 1) * region, (int)roff[q * 2 + 1], s.pipe_part + (q * 2) * region,
-        (int)roff[q * 2], s.records + q * NTERMS);
-    ctx->launches++;
+  for (int si = 0; si < ns; ++si) {
+    Slab& s = ctx->slabs[si];
+    CK(cudaSetDevice(s.dev));
+    for (int64_t q = 0; q <= nrec; ++q) {
+      finalize_terms<<<1, kThreads, 0, s.stream>>>(
+          s.pipe_part + (q * 2 + 1) * region, (int)roff[si][q * 2 + 1],
+          s.pipe_part + (q * 2) * region, (int)roff[si][q * 2], s.records + q * NTERMS);
+      ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s.ev_done, s.dstream));
+    CK(cudaStreamWaitEvent(s.stream, s.ev_done, 0));
+    CK(cudaEventRecord(s.ev_bnd, s.stream));
   }
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(s.ev_done, s.dstream));
-  CK(cudaStreamWaitEvent(s.stream, s.ev_done, 0));
-  CK(cudaEventRecord(s.ev_t1, s.stream));
+  CK(cudaSetDevice(s0.dev));
+  for (Slab& s : ctx->slabs) CK(cudaStreamWaitEvent(s0.stream, s.ev_bnd, 0));
+  CK(cudaEventRecord(s0.ev_t1, s0.stream));
   r = sync_all(ctx);
-  if (!r) CK(cudaStreamSynchronize(s.dstream));
   if (r) return r;
+  for (Slab& s : ctx->slabs) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.dstream));
+    CK(cudaStreamSynchronize(s.ustream));
+  }
+  for (Slab& s : ctx->slabs) s.xch_pending = false;   // synchronised above
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, s.ev_t0, s.ev_t1));
+  CK(cudaSetDevice(s0.dev));
+  CK(cudaEventElapsedTime(&ms, s0.ev_t0, s0.ev_t1));
   ctx->last_ms = ms;
   return read_bad(ctx, bad_out);
 }

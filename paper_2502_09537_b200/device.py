@@ -13,6 +13,7 @@ arrays are updated in place like the reference's in-place sweeps).
 from __future__ import annotations
 
 import ctypes
+import os
 from collections import OrderedDict
 
 import numpy as np
@@ -80,7 +81,14 @@ class DeviceContext:
         ptr = ctypes.c_void_p()
         if self.dist:
             p = self.plan
-            nid = make_nccl_id(p.rank, _torch_broadcast) if p.world_size > 1 else None
+            if p.world_size > 1:
+                nid = make_nccl_id(p.rank, _torch_broadcast)
+            elif os.environ.get("KGS_SELF_EXCHANGE") == "1":
+                # test hook: one rank exchanging its faces with itself over
+                # NCCL -- the multi-rank code path on one GPU (kgs_b200.h)
+                nid = make_nccl_id(0, lambda obj: obj)
+            else:
+                nid = None
             rc = lib.kgs_create_dist(grid.d, grid.N, grid.a, grid.b, p.rank,
                                      p.world_size, p.device, nid, ctypes.byref(ptr))
         else:
@@ -178,7 +186,7 @@ class DeviceContext:
         upload, nsteps DP-AVF2 steps and download overlapped in a pipeline;
         the host arrays are updated in place.  Returns (terms0, terms[nrec, 8],
         bad_step); on a non-finite step the state is the one after `bad_step`."""
-        if self.dist:
+        if self.dist and self.plan.world_size > 1:
             raise ValueError("integrate_host is for single-process contexts")
         lib = _lib.load()
         c = _lib.coeffs_struct(kernel_args)

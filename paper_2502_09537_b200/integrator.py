@@ -239,8 +239,9 @@ def integrate(state, grid: GridSpec, params: PhysParams,
 
     if host is not None and not snap and n_steps > 0 and _pipeline_ok(host, grid):
         ctx = get_context(grid, executor)
-        if not ctx.dist:
-            # one call: upload | steps | download overlapped (kgs_integrate_host)
+        if not ctx.dist or ctx.plan.world_size == 1:
+            # one call: upload | steps | download overlapped (kgs_integrate_host;
+            # several slabs run the pipeline side by side with face exchanges)
             t_start = state.t
             terms0, terms, bad = ctx.integrate_host(host, args, n_steps, record_stride)
             e0, m0 = energy_from_terms(terms0, params, grid)

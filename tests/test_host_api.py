@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.kgs_abi_version() == 101
+    assert lib.kgs_abi_version() == 102
     assert lib.kgs_build_flags() == 0   # the default library: no experimental code, no asserts
 
 
@@ -95,8 +95,8 @@ def test_null_arguments_are_rejected_without_touching_a_device():
     assert lib.kgs_destroy(None) == _lib.KGS_OK
     assert lib.kgs_launch_count(None) == 0
     # the plan query validates its output buffer too
-    assert lib.kgs_pipeline_plan(64, 8, 2, None, 10) == -1
-    assert lib.kgs_pipeline_plan(64, 8, 2, None, 0) > 0
+    assert lib.kgs_pipeline_plan(64, 8, 2, 0, None, 10) == -1
+    assert lib.kgs_pipeline_plan(64, 8, 2, 0, None, 0) > 0
 
 
 @pytest.mark.skipif(_have_gpu(), reason="checks the no-GPU failure path")
