@@ -21,6 +21,8 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -49,6 +51,7 @@ bool load_nccl(std::string& err) {
   KGS_SYM(Recv, "ncclRecv");
   KGS_SYM(GroupStart, "ncclGroupStart");
   KGS_SYM(GroupEnd, "ncclGroupEnd");
+  KGS_SYM(AllReduce, "ncclAllReduce");
   KGS_SYM(GetErrorString, "ncclGetErrorString");
 #undef KGS_SYM
   g_nccl.ok = true;
@@ -118,6 +121,7 @@ struct kgs_ctx {
   // (KGS_SELF_EXCHANGE=1 test hook, kgs_create_dist): the multi-rank path on one GPU
   bool self_xch = false;
   ncclComm_t comm = nullptr;
+  unsigned long long* dword = nullptr;   // device word for rank agreements (rank_min)
   std::string err = "no error";
   std::atomic<int64_t> launches{0};   // our kernel launches (the pipeline uploader thread adds too)
   double last_ms = 0.0;

@@ -185,6 +185,10 @@ int kgs_create_dist(int d, int64_t N, double a, double b, int rank, int nranks,
 int kgs_destroy(kgs_ctx* ctx) {
   if (!ctx) return KGS_OK;
   if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->dword) {
+    cudaSetDevice(ctx->slabs.empty() ? 0 : ctx->slabs[0].dev);
+    cudaFree(ctx->dword);
+  }
   for (auto e : ctx->pass_ev) cudaEventDestroy(e);
   for (auto& s : ctx->slabs) {
     cudaSetDevice(s.dev);
@@ -573,7 +577,10 @@ int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
     int64_t fb = 0;
     r = kgs_step_dpavf2(ctx, half, nsteps, step_offset, record_stride, terms_out, &fb, 0);
     if (r && r != KGS_ENONFINITE) return r;
-    if (r == KGS_ENONFINITE) {   // replay from the (untouched) host state to the bad step
+    unsigned long long b = r == KGS_ENONFINITE ? (unsigned long long)fb : ULLONG_MAX;
+    if (int e = rank_min(ctx, &b)) return e;   // the ranks replay to the same step
+    fb = (int64_t)b;
+    if (b != ULLONG_MAX) {   // replay from the (untouched) host state to the bad step
       int r2 = kgs_upload(ctx, P, Q, U, V);
       int64_t fb2 = 0;
       if (!r2 && fb > step_offset)

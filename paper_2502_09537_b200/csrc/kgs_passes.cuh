@@ -78,6 +78,20 @@ int exchange(kgs_ctx* ctx, int col) {
   return KGS_OK;
 }
 
+// Ranks of a torchrun job agree on a value: the minimum over ranks (an NCCL
+// all-reduce every rank must reach at the same point).  Otherwise a no-op.
+int rank_min(kgs_ctx* ctx, unsigned long long* v) {
+  if (!(ctx->dist && ctx->nranks > 1)) return KGS_OK;
+  Slab& s = ctx->slabs[0];
+  CK(cudaSetDevice(s.dev));
+  if (!ctx->dword) CK(cudaMalloc(&ctx->dword, sizeof(unsigned long long)));
+  CK(cudaMemcpyAsync(ctx->dword, v, sizeof *v, cudaMemcpyHostToDevice, s.cstream));
+  NK(g_nccl.AllReduce(ctx->dword, ctx->dword, 1, ncclUint64, ncclMin, ctx->comm, s.cstream));
+  CK(cudaMemcpyAsync(v, ctx->dword, sizeof *v, cudaMemcpyDeviceToHost, s.cstream));
+  CK(cudaStreamSynchronize(s.cstream));
+  return KGS_OK;
+}
+
 int finalize_record(kgs_ctx* ctx, int64_t slot, bool both);
 
 int sync_all(kgs_ctx* ctx) {

@@ -274,67 +274,75 @@ int ensure_host_slots(kgs_ctx* ctx, Slab& s, int64_t slot) {
 int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, int64_t nsteps,
                         int64_t step_offset, int64_t record_stride, int64_t nrec,
                         unsigned long long* bad_out) {
-  if (!ctx->tune_pipe || ctx->d != 3) return kPipeFallback;
   const int ns = (int)ctx->slabs.size();
   // several slabs / ranks: every slab runs the same plan on its own planes,
   // with face exchanges between the passes (pipeline_plan)
   const bool split = needs_exchange(ctx);
   const int64_t N = ctx->slabs[0].nx;   // planes per slab
-  for (const Slab& s : ctx->slabs)
-    if (s.nx != N) return kPipeFallback;
   // chunk planes; a layout-transform launch covers < 2^31 point pairs (decode_point)
   const int64_t C = std::max<int64_t>(1, std::min<int64_t>(ctx->tune_pipe_chunk,
                                                            ((1ll << 31) - 1) / ((int64_t)ctx->ny * ctx->nk)));
   const int64_t nb = (N + C - 1) / C;
-  if (nb < 4) return kPipeFallback;
   const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
+  const int64_t stage = 4 * C * nat_plane;
+  const int64_t maxl = nb + 4;                                 // launches per pass
+  const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
+  const int64_t need = (nrec + 1) * 2 * region;
   // pageable arrays (the reference's numpy FieldState): staged through
   // page-locked slots by host threads -- one slab's pipeline; several slabs
   // take the plain path for them.  Page-locked arrays (FieldState.pinned) go direct.
   bool staged = false;
   if (ctx->tune_stage)
     for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
-  if (staged && ns > 1) return kPipeFallback;
-  if (ensure_alt(ctx)) return kPipeFallback;
-  const int64_t stage = 4 * C * nat_plane;
-  const int64_t maxl = nb + 4;                                 // launches per pass
-  const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
-  const int64_t need = (nrec + 1) * 2 * region;
-  if (need > (int64_t)1 << 27) return kPipeFallback;           // > 1 GiB of partials per slab
-  for (Slab& s : ctx->slabs) {
-    CK(cudaSetDevice(s.dev));
-    if (s.pipe_stage < stage) {
-      if (s.pipe_up) CK(cudaFree(s.pipe_up));
-      if (s.pipe_dn) CK(cudaFree(s.pipe_dn));
-      s.pipe_up = s.pipe_dn = nullptr;
-      s.pipe_stage = 0;
-      if (cudaMalloc(&s.pipe_up, stage * 8) != cudaSuccess ||
-          cudaMalloc(&s.pipe_dn, stage * 8) != cudaSuccess) {
-        cudaGetLastError();
-        if (s.pipe_up) cudaFree(s.pipe_up);
-        s.pipe_up = nullptr;
-        return kPipeFallback;
+  // eligibility and buffers; the ranks of a torchrun job then agree, so all
+  // of them run the pipeline (with its exchanges) or none does
+  auto prepare = [&]() -> int {
+    if (!ctx->tune_pipe || ctx->d != 3 || nb < 4 || (staged && ns > 1)) return kPipeFallback;
+    for (const Slab& s : ctx->slabs)
+      if (s.nx != N) return kPipeFallback;
+    if (need > (int64_t)1 << 27) return kPipeFallback;         // > 1 GiB of partials per slab
+    if (ensure_alt(ctx)) return kPipeFallback;
+    for (Slab& s : ctx->slabs) {
+      CK(cudaSetDevice(s.dev));
+      if (s.pipe_stage < stage) {
+        if (s.pipe_up) CK(cudaFree(s.pipe_up));
+        if (s.pipe_dn) CK(cudaFree(s.pipe_dn));
+        s.pipe_up = s.pipe_dn = nullptr;
+        s.pipe_stage = 0;
+        if (cudaMalloc(&s.pipe_up, stage * 8) != cudaSuccess ||
+            cudaMalloc(&s.pipe_dn, stage * 8) != cudaSuccess) {
+          cudaGetLastError();
+          if (s.pipe_up) cudaFree(s.pipe_up);
+          s.pipe_up = nullptr;
+          return kPipeFallback;
+        }
+        s.pipe_stage = stage;
       }
-      s.pipe_stage = stage;
-    }
-    if (s.pipe_part_cap < need) {
-      if (s.pipe_part) CK(cudaFree(s.pipe_part));
-      s.pipe_part = nullptr;
-      s.pipe_part_cap = 0;
-      if (cudaMalloc(&s.pipe_part, need * 8) != cudaSuccess) {
-        cudaGetLastError();
-        return kPipeFallback;
+      if (s.pipe_part_cap < need) {
+        if (s.pipe_part) CK(cudaFree(s.pipe_part));
+        s.pipe_part = nullptr;
+        s.pipe_part_cap = 0;
+        if (cudaMalloc(&s.pipe_part, need * 8) != cudaSuccess) {
+          cudaGetLastError();
+          return kPipeFallback;
+        }
+        s.pipe_part_cap = need;
       }
-      s.pipe_part_cap = need;
+      if (!s.dstream) CK(cudaStreamCreateWithFlags(&s.dstream, cudaStreamNonBlocking));
+      if (!s.ustream) CK(cudaStreamCreateWithFlags(&s.ustream, cudaStreamNonBlocking));
+      while ((int64_t)s.pipe_ev.size() < 2 * nb) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s.pipe_ev.push_back(e);
+      }
     }
-    if (!s.dstream) CK(cudaStreamCreateWithFlags(&s.dstream, cudaStreamNonBlocking));
-    if (!s.ustream) CK(cudaStreamCreateWithFlags(&s.ustream, cudaStreamNonBlocking));
-    while ((int64_t)s.pipe_ev.size() < 2 * nb) {
-      cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      s.pipe_ev.push_back(e);
-    }
-  }
+    return KGS_OK;
+  };
+  const int pr = prepare();
+  unsigned long long go = pr == KGS_OK ? 1 : 0;
+  if (int e = rank_min(ctx, &go)) return e;
+  if (pr) return pr;                  // an error, or this rank's fallback
+  if (!go) return kPipeFallback;      // another rank cannot run it
   int r = ensure_records(ctx, nrec + 1);
   if (!r) r = reset_bad(ctx);
   if (r) return r;
@@ -657,7 +665,9 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   CK(cudaSetDevice(s0.dev));
   CK(cudaEventElapsedTime(&ms, s0.ev_t0, s0.ev_t1));
   ctx->last_ms = ms;
-  return read_bad(ctx, bad_out);
+  r = read_bad(ctx, bad_out);
+  if (!r) r = rank_min(ctx, bad_out);   // every rank replays to the same step
+  return r;
 }
 
 }  // namespace

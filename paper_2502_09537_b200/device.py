@@ -186,20 +186,26 @@ class DeviceContext:
         upload, nsteps DP-AVF2 steps and download overlapped in a pipeline;
         the host arrays are updated in place.  Returns (terms0, terms[nrec, 8],
         bad_step); on a non-finite step the state is the one after `bad_step`."""
-        if self.dist and self.plan.world_size > 1:
-            raise ValueError("integrate_host is for single-process contexts")
         lib = _lib.load()
         c = _lib.coeffs_struct(kernel_args)
         nrec = nsteps // record_stride if record_stride > 0 else 0
         terms0 = np.zeros(_lib.NTERMS)
         terms = np.zeros((max(nrec, 1), _lib.NTERMS))
         bad = ctypes.c_int64(0)
-        rc = lib.kgs_integrate_host(self.ptr, *(_lib.dptr(getattr(state, f)) for f in "PQUV"),
+        # this context's planes (a rank: its slab of a whole-grid array, or its own slab)
+        views = [self.local(getattr(state, f)) for f in "PQUV"]
+        rc = lib.kgs_integrate_host(self.ptr, *(_lib.dptr(v) for v in views),
                                     ctypes.byref(c), nsteps, 0, record_stride,
                                     _lib.dptr(terms0), _lib.dptr(terms), ctypes.byref(bad), 0)
         if rc not in (_lib.KGS_OK, _lib.KGS_ENONFINITE):
             self.check(rc)
-        return terms0, terms[:nrec], (bad.value if rc == _lib.KGS_ENONFINITE else 0)
+        terms = terms[:nrec]
+        if self.dist and self.plan.world_size > 1:   # per-rank sums, added in rank order
+            gathered = _torch_allgather((terms0, terms))
+            terms0 = combine_rank_terms([t0 for t0, _ in gathered])
+            terms = sum((np.asarray(t) for _, t in gathered[1:]), np.asarray(gathered[0][1]))
+        # the library makes the ranks agree on the first bad step
+        return terms0, terms, (bad.value if rc == _lib.KGS_ENONFINITE else 0)
 
     def step_dpavf2(self, kernel_args, nsteps: int, step_offset: int = 0,
                     record_stride: int = 0, defer_tail: bool = False, backup: bool = False):

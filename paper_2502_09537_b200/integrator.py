@@ -141,15 +141,26 @@ class EnergyTrace:
         return max(self.rel_error)
 
 
-def _pipeline_ok(host, grid: GridSpec) -> bool:
+def _pipeline_ok(host, sizes) -> bool:
     """The one-call path hands the host arrays to C as raw pointers: they must
-    be whole-grid, contiguous, writable float64 (else the checked path runs)."""
+    be contiguous, writable float64 of one of `sizes` (the whole grid, or a
+    rank's own slab) -- else the checked path runs."""
     for f in "PQUV":
         a = getattr(host, f)
-        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.shape == (grid.M,)
-                and a.flags["C_CONTIGUOUS"] and a.flags["WRITEABLE"]):
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.ndim == 1
+                and a.size in sizes and a.flags["C_CONTIGUOUS"] and a.flags["WRITEABLE"]):
             return False
     return True
+
+
+def _one_call_ok(ctx, host, grid: GridSpec) -> bool:
+    """The host arrays suit kgs_integrate_host; the ranks of a torchrun job
+    agree on it (the call's halo exchanges are collective)."""
+    ok = _pipeline_ok(host, (grid.M, ctx.points) if ctx.dist else (grid.M,))
+    if ctx.dist and ctx.plan.world_size > 1:
+        from .device import _torch_allgather
+        ok = all(_torch_allgather(ok))
+    return ok
 
 
 def _append_records(trace, terms, k0, k1, record_stride, t, e0, absolute, params, grid,
@@ -237,23 +248,23 @@ def integrate(state, grid: GridSpec, params: PhysParams,
             t += coeffs_half.tau
         return t
 
-    if host is not None and not snap and n_steps > 0 and _pipeline_ok(host, grid):
-        ctx = get_context(grid, executor)
-        if not ctx.dist or ctx.plan.world_size == 1:
-            # one call: upload | steps | download overlapped (kgs_integrate_host;
-            # several slabs run the pipeline side by side with face exchanges)
-            t_start = state.t
-            terms0, terms, bad = ctx.integrate_host(host, args, n_steps, record_stride)
-            e0, m0 = energy_from_terms(terms0, params, grid)
-            absolute = abs(e0) < 1e-300
-            trace = EnergyTrace([0], [t_start], [e0], [0.0], [m0], re_is_absolute=absolute)
-            if bad:
-                state.t = advance_t(t_start, bad)
-                raise FloatingPointError(
-                    f"non-finite field values detected after step {bad} (t={state.t})")
-            state.t = _append_records(trace, terms, 1, n_steps, record_stride, t_start, e0,
-                                      absolute, params, grid, advance_t)
-            return trace
+    ctx = get_context(grid, executor) if host is not None and not snap and n_steps > 0 else None
+    if ctx is not None and _one_call_ok(ctx, host, grid):
+        # one call: upload | steps | download overlapped (kgs_integrate_host;
+        # several slabs or ranks run the pipeline side by side with face
+        # exchanges; every rank of a torchrun job makes this same call)
+        t_start = state.t
+        terms0, terms, bad = ctx.integrate_host(host, args, n_steps, record_stride)
+        e0, m0 = energy_from_terms(terms0, params, grid)
+        absolute = abs(e0) < 1e-300
+        trace = EnergyTrace([0], [t_start], [e0], [0.0], [m0], re_is_absolute=absolute)
+        if bad:
+            state.t = advance_t(t_start, bad)
+            raise FloatingPointError(
+                f"non-finite field values detected after step {bad} (t={state.t})")
+        state.t = _append_records(trace, terms, 1, n_steps, record_stride, t_start, e0,
+                                  absolute, params, grid, advance_t)
+        return trace
 
     dev, _ = as_device_state(state, grid, executor)
 

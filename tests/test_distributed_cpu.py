@@ -336,3 +336,131 @@ def test_step_program_structure():
     assert d[-2, 0] == _lib.PG_DEFER
     h = _lib.step_program(6, False, 1, 2, 0, head_fused=True)
     assert h[1, 1:4].tolist() == [1, OP_ADJ, OP_BASE]
+
+
+# ---- the pipelined integrate (kgs_integrate_host) on several ranks --------
+# Every rank runs the split pipeline plan (kgs_pipeline_plan(..., split=1),
+# the list the device executor issues): chunks arrive in folded order, passes
+# cover plane ranges as a wavefront, faces are exchanged after each writing
+# pass has covered both boundary planes, a launch touching a boundary plane
+# first takes delivery of pending exchanges (the device: the compute stream
+# waits for the exchange event), and FINAL blocks are copied out at once --
+# they must already hold the end state.
+
+PIPE_ARRIVE, PIPE_PASS, PIPE_FINAL, PIPE_XCH = 0, 1, 2, 3
+
+
+def pipeline_events(nx, C, nsteps):
+    import ctypes
+    lib = _lib.load()
+    n = lib.kgs_pipeline_plan(nx, C, nsteps, 1, None, 0)
+    buf = (ctypes.c_int64 * (4 * n))()
+    assert lib.kgs_pipeline_plan(nx, C, nsteps, 1, buf, n) == n
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(n)]
+
+
+def pipeline_passes(nsteps):
+    """(colour, op1, op2) of every pass, as integrate_pipelined builds them."""
+    p = [(0, OP_NONE, OP_NONE), (1, OP_NONE, OP_NONE), (1, OP_BASE, OP_NONE)]
+    for i in range(1, nsteps + 1):
+        p += [(0, OP_BASE, OP_ADJ), (1, OP_ADJ, OP_BASE if i < nsteps else OP_NONE)]
+    return p
+
+
+class PipeReplay(SlabReplay):
+    """One rank executing the split pipeline plan: nothing has arrived at
+    the start (local planes and ghosts NaN)."""
+
+    def __init__(self, grid, state, rank, world, args, lazy):
+        super().__init__(grid, state, rank, world, args, lazy)
+        self.host = {n: self.f[n][1:-1].copy() for n in "PQUV"}
+        for n in "PQUV":
+            self.f[n][:] = np.nan
+        self.finals = {}
+
+    def run_plan(self, events, passes):
+        for kind, idx, a, b in events:
+            if kind == PIPE_ARRIVE:
+                for n in "PQUV":
+                    self.f[n][a + 1:b + 1] = self.host[n][a:b]
+            elif kind == PIPE_XCH:
+                cols = (0, 1) if idx < 0 else (passes[idx][0],)
+                for c in cols:
+                    if self.lazy:
+                        self.pending.append(c)
+                    else:
+                        self._exchange(c)
+            elif kind == PIPE_PASS:
+                if self.pending and (a == 0 or b == self.nx):
+                    for c in self.pending:
+                        self._exchange(c)
+                    self.pending = []
+                col, op1, op2 = passes[idx]
+                self._launch(col, op1, op2, False, a, b)
+            elif kind == PIPE_FINAL:
+                self.finals[(a, b)] = {n: self.f[n][a + 1:b + 1].copy() for n in "PQUV"}
+            else:
+                raise AssertionError(f"unknown pipeline event {kind}")
+        for c in self.pending:   # the last exchanges (ghosts for later calls)
+            self._exchange(c)
+        self.pending = []
+
+
+def _pipe_worker(rank, world, port, N, C, nsteps, lazy, out, drop_xch=False):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid = GridSpec(3, -1.0, 1.0, N)
+        s = seeded_random_state(grid, 42, 0.5)
+        args = oracle.kernel_args(PARAMS, 0.02, grid)
+        rep = PipeReplay(grid, s, rank, world, args, lazy)
+        events = pipeline_events(rep.nx, C, nsteps)
+        if drop_xch:   # mutation: the faces of the first K3 never travel
+            events = [e for e in events if not (e[0] == PIPE_XCH and e[1] == 3)]
+        rep.run_plan(events, pipeline_passes(nsteps))
+        out.put((rank, rep.x0, {n: rep.f[n][1:-1].copy() for n in "PQUV"}, rep.finals))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_pipe_world(world, N, C, nsteps, lazy, drop_xch=False):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_worker,
+                         args=(r, world, port, N, C, nsteps, lazy, q, drop_xch))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return results
+
+
+@pytest.mark.parametrize("lazy", [False, True], ids=["eager", "lazy"])
+@pytest.mark.parametrize("world,N,C,nsteps", [
+    (2, 16, 2, 2), (2, 16, 3, 3), (4, 16, 1, 2), (2, 12, 1, 1), (4, 24, 2, 3)])
+def test_pipeline_plan_replayed_over_gloo_is_bitwise(world, N, C, nsteps, lazy):
+    results = _run_pipe_world(world, N, C, nsteps, lazy)
+    grid, ref, _ = _reference(N, nsteps, set())
+    full = {f: getattr(ref, f).reshape(grid.shape) for f in "PQUV"}
+    for rank, x0, fields, finals in results:
+        nx = fields["P"].shape[0]
+        assert sorted(finals) == [(a, min(a + C, nx)) for a in range(0, nx, C)]
+        for f in "PQUV":
+            assert np.array_equal(fields[f], full[f][x0:x0 + nx]), (rank, f)
+            for (a, b), blk in finals.items():   # copied back = the end state
+                assert np.array_equal(blk[f], full[f][x0 + a:x0 + b]), (rank, f, a)
+
+
+def test_pipeline_replay_detects_a_missing_exchange():
+    """Sanity of the replay: without one pass's face exchange the ghosts
+    hold stale faces and the fields are no longer the oracle's."""
+    results = _run_pipe_world(2, 16, 2, 2, lazy=False, drop_xch=True)
+    grid, ref, _ = _reference(16, 2, set())
+    full = {f: getattr(ref, f).reshape(grid.shape) for f in "PQUV"}
+    same = all(np.array_equal(fields[f], full[f][x0:x0 + fields[f].shape[0]])
+               for _, x0, fields, _ in results for f in "PQUV")
+    assert not same

@@ -313,21 +313,26 @@ def test_device_count_comes_from_the_library():
 
 def test_one_call_path_only_takes_whole_grid_writable_float64():
     """integrate() hands host arrays to kgs_integrate_host as raw pointers;
-    anything else must take the shape-checked path."""
+    anything else must take the shape-checked path (sizes: the whole grid, or
+    for a torchrun rank also its own slab)."""
     from paper_2502_09537_b200.integrator import _pipeline_ok
     g = kgs.GridSpec(2, 0.0, 1.0, 8)
     s = kgs.FieldState.zeros(g)
-    assert _pipeline_ok(s, g)
-    assert not _pipeline_ok(s, kgs.GridSpec(2, 0.0, 1.0, 16))      # too small for the grid
+    assert _pipeline_ok(s, (g.M,))
+    assert not _pipeline_ok(s, (kgs.GridSpec(2, 0.0, 1.0, 16).M,))   # too small for the grid
+    assert _pipeline_ok(s, (4 * g.M, g.M))                           # a rank's own slab
     bad = kgs.FieldState.zeros(g)
     bad.U = np.zeros(2 * g.M)[::2]                                   # strided view
-    assert not _pipeline_ok(bad, g)
+    assert not _pipeline_ok(bad, (g.M,))
     ro = kgs.FieldState.zeros(g)
     ro.V.flags.writeable = False
-    assert not _pipeline_ok(ro, g)
+    assert not _pipeline_ok(ro, (g.M,))
     f32 = kgs.FieldState.zeros(g)
     f32.P = np.zeros(g.M, dtype=np.float32)
-    assert not _pipeline_ok(f32, g)
+    assert not _pipeline_ok(f32, (g.M,))
+    two_d = kgs.FieldState.zeros(g)
+    two_d.Q = np.zeros((g.N, g.N))
+    assert not _pipeline_ok(two_d, (g.M,))
 
 
 @pytest.mark.parametrize("name,N,block", [("ellipsoids3d", 48, 1000), ("ellipsoids3d", 64, 1 << 22),
