@@ -784,6 +784,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   }
   else if (n == "march_planes") ctx->tune_xc = value;
   else if (n == "blocks_per_sm") ctx->tune_occ = value;
+  else if (n == "march_sms") ctx->tune_sms = value;
   else if (n == "fused_step") {
 #ifndef KGS_EXPERIMENTAL
     if (value) return fail(ctx, KGS_EINVAL, "fused_step needs a -DKGS_EXPERIMENTAL build");

@@ -235,7 +235,8 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
     }
   }
   const int bps = ctx->tune_occ > 0 ? std::min(occ, ctx->tune_occ) : occ;
-  int64_t G = std::min<int64_t>((int64_t)bps * ctx->nsm, ctx->grid_cap);
+  const int sms = ctx->tune_sms > 0 ? std::min(ctx->nsm, ctx->tune_sms) : ctx->nsm;
+  int64_t G = std::min<int64_t>((int64_t)bps * sms, ctx->grid_cap);
   if (CL > 1) G = std::min<int64_t>(G, (int64_t)max_clusters * CL) / CL * CL;
   const int64_t cols = (int64_t)(g.ny / Var::TY) * (g.nk / Var::TK);
   const int nxr = g.xb - g.xa;

@@ -27,7 +27,7 @@ sc = kgs.get_scenario("ellipsoids3d")
 g = sc.default_grid(a.N)
 dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
 args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
-defaults = {"march_wave_sync": 0, "march_planes": 0, "march_variant": 4}
+defaults = {"march_wave_sync": 1, "march_planes": 0, "march_variant": 4, "march_sms": 0, "blocks_per_sm": 0}
 off = 0
 dev.ctx.step_dpavf2(args, 2, off, 0)
 off += 2
