@@ -3,6 +3,7 @@
 must come out bitwise identical for every setting.
 
     python tools/knob_ab.py KNOB V0,V1[,..] [--N 1024] [--steps 6] [--reps 4] [--call]
+                            [--scenario fourpeak2d]
 
 --call times the whole kgs_step_dpavf2 call (host wall clock around the
 synchronous call, one untimed warm-up call first) instead of the per-pass
@@ -27,16 +28,17 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--call", action="store_true")
+    ap.add_argument("--scenario", default="ellipsoids3d")
     a = ap.parse_args()
     vals = [int(v) for v in a.values.split(",")]
-    sc = kgs.get_scenario("ellipsoids3d")
+    sc = kgs.get_scenario(a.scenario)
     g = sc.default_grid(a.N)
     args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
     times = {v: [] for v in vals}
     digests = {}
     for rep in range(a.reps):
         for v in vals:
-            dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
+            dev = kgs.DeviceFieldState.from_preset(a.scenario, g)
             dev.ctx.set_param(a.knob, v)
             if a.call:
                 dev.ctx.step_dpavf2(args, 2, 0, 2)
@@ -59,7 +61,7 @@ def main():
     out = {str(v): {key: [round(t, 4) for t in times[v]],
                     "mean": round(sum(times[v]) / len(times[v]), 4)} for v in vals}
     out["bitwise_equal"] = len(set(digests.values())) == 1
-    print(json.dumps({"knob": a.knob, "N": a.N, **out}))
+    print(json.dumps({"knob": a.knob, "scenario": a.scenario, "N": a.N, **out}))
 
 
 if __name__ == "__main__":
