@@ -194,3 +194,42 @@ def test_random_operation_sequences_resident_vs_passes(d, seed, ops):
         dev.close()
     assert_bitwise(outs[0][0], outs[1][0])
     np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-12, atol=1e-300)
+
+
+@SETTINGS
+@given(N=st.sampled_from([64, 96, 128]), slabs=st.sampled_from([2, 4]),
+       planes=st.integers(1, 12), steps=st.integers(1, 7), stride=st.integers(1, 4),
+       seed=st.integers(0, 2**31), tau=st.floats(1e-3, 0.05),
+       poison=st.one_of(st.none(), st.integers(0, 127)))
+def test_slab_pipeline_equals_one_slab(N, slabs, planes, steps, stride, seed, tau, poison):
+    """The pipelined integrate on several slabs (face exchanges between the
+    passes, pinned host arrays) against one slab's pipeline: same fields,
+    same records to summation order, same first bad step."""
+    if (N // slabs) // planes < 4:
+        planes = max(1, (N // slabs) // 4)       # the pipeline needs >= 4 chunks per slab
+    g = kgs.GridSpec(3, -6.0, 6.0, N)
+    p = kgs.PhysParams(1.0, 0.8, 1.1, 0.9)
+    s0 = _state(g, seed)
+    if poison is not None:
+        s0.Q[(poison % N) * N * N + 7] = np.inf
+    outs = []
+    for ex in (None, kgs.CudaExecutor((0,), slabs_per_device=slabs)):
+        ctx = get_context(g, ex)
+        ctx.set_param("pipeline_planes", planes)
+        s = kgs.FieldState.pinned(g)
+        for f in "PQUV":
+            getattr(s, f)[:] = getattr(s0, f)
+        try:
+            tr = kgs.integrate(s, g, p, kgs.checkerboard_schedule(g), ex, tau, steps * tau,
+                               record_stride=stride)
+            outs.append((s.copy(), tr.energy, None))
+        except FloatingPointError as e:
+            outs.append((s.copy(), None, str(e)))
+        ctx.set_param("pipeline_planes", 32)
+    (a, ea, xa), (b, eb, xb) = outs
+    assert xa == xb
+    for f in "PQUV":
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+    assert a.t == b.t
+    if ea is not None:
+        np.testing.assert_allclose(ea, eb, rtol=1e-12, atol=1e-300)
