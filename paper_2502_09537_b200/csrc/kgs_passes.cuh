@@ -79,9 +79,11 @@ int exchange(kgs_ctx* ctx, int col) {
 }
 
 // Ranks of a torchrun job agree on a value: the minimum over ranks (an NCCL
-// all-reduce every rank must reach at the same point).  Otherwise a no-op.
+// all-reduce every rank must reach at the same point).  Otherwise a no-op --
+// except for a self-exchanging rank (KGS_SELF_EXCHANGE), which runs the
+// 1-rank all-reduce so that this path executes on one GPU too.
 int rank_min(kgs_ctx* ctx, unsigned long long* v) {
-  if (!(ctx->dist && ctx->nranks > 1)) return KGS_OK;
+  if (!(ctx->dist && (ctx->nranks > 1 || ctx->self_xch))) return KGS_OK;
   Slab& s = ctx->slabs[0];
   CK(cudaSetDevice(s.dev));
   if (!ctx->dword) CK(cudaMalloc(&ctx->dword, sizeof(unsigned long long)));

@@ -101,3 +101,29 @@ def test_rank_pipeline_with_nccl_self_exchange(monkeypatch):
     assert na > 0 and n1 > 0
     assert_bitwise(a, one)
     np.testing.assert_allclose(ta.energy, t1.energy, rtol=1e-13, atol=0)
+
+
+def test_rank_pipeline_nonfinite_agrees_and_replays(monkeypatch):
+    """The rank path's agreement on the first bad step (an NCCL all-reduce,
+    run here by one self-exchanging rank) and its replay: same state and
+    message as one ordinary slab."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(128)
+    s0 = sc.state(g)
+    s0.P[127 * 128 * 128 + 9] = np.nan     # the last plane: a face of the rank
+    out = {}
+    for key, selfx in (("rank", True), ("one", False)):
+        if selfx:
+            monkeypatch.setenv("KGS_SELF_EXCHANGE", "1")
+        else:
+            monkeypatch.delenv("KGS_SELF_EXCHANGE", raising=False)
+        kgs.clear_contexts()
+        ex = kgs.DistributedExecutor(rank=0, world_size=1, device=0) if selfx else None
+        get_context(g, ex).set_param("pipeline_planes", 8)
+        s = _pinned_copy(g, s0)
+        with pytest.raises(FloatingPointError) as ei:
+            kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), ex, 0.01, 0.04,
+                          record_stride=1)
+        out[key] = (s, str(ei.value))
+    assert_bitwise(out["rank"][0], out["one"][0], equal_nan=True)
+    assert out["rank"][1] == out["one"][1]
