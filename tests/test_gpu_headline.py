@@ -9,7 +9,8 @@ through the exact call pattern bench.py times:
     step (bench diagnostics) -- the plain, end-record and every-step-record
     march_pass variants;
   * public API: ``integrate()`` on a host FieldState (the pipelined
-    upload | passes | download path bench's e2e times).
+    upload | passes | download path bench's e2e times), and the same on two
+    slabs from page-locked memory (the multi-slab pipeline).
 
 Both are compared bit for bit with the table-free C restatement
 (oracle/kgs_oracle.c, pinned to the reference's golden vectors in
@@ -17,7 +18,7 @@ tests/test_oracle_golden.py) run for the same 20 steps on all host cores;
 the recorded energy terms are checked against the oracle's exactly-summed
 terms, and energy conservation at the reference's round-off level.
 
-Host memory: ~70 GB (oracle state, integrate() state, chunk buffers); the
+Host memory: ~105 GB (oracle state, two integrate() states, chunk buffers); the
 oracle takes ~1 min on 16 cores.
 """
 from __future__ import annotations
@@ -80,6 +81,17 @@ def test_headline_1024_bitwise_vs_oracle():
     assert tr.steps == [0, 5, 10, 15, 20]
     kgs.clear_contexts()
 
+    # ---- integrate() on two slabs: the multi-slab pipeline (faces exchanged
+    # between the passes) from page-locked host memory ---------------------
+    host2 = kgs.FieldState.pinned(g, zero=False)
+    for f in "PQUV":
+        getattr(host2, f)[:] = getattr(ref, f)
+    ex2 = kgs.CudaExecutor((0,), slabs_per_device=2)
+    tr2 = kgs.integrate(host2, g, sc.params, kgs.checkerboard_schedule(g), ex2,
+                        TAU, STEPS * TAU, record_stride=5)
+    np.testing.assert_allclose(tr2.energy, tr.energy, rtol=1e-13, atol=0)
+    kgs.clear_contexts()
+
     # ---- oracle: 20 steps on the host, all cores -------------------------
     orc = oracle.TableFreeOracle(3, N)
     terms0 = orc.energy_terms(ref)
@@ -88,11 +100,12 @@ def test_headline_1024_bitwise_vs_oracle():
     # fields: bitwise, both paths
     _compare_device(dev, ref)
     dev.close()
-    for f in "PQUV":
-        a, b = getattr(host, f), getattr(ref, f)
-        if not np.array_equal(a, b):
-            bad = np.flatnonzero(a != b)
-            raise AssertionError(f"integrate() {f}: {bad.size} mismatches, first at {bad[0]}")
+    for label, st in (("integrate()", host), ("integrate() on 2 slabs", host2)):
+        for f in "PQUV":
+            a, b = getattr(st, f), getattr(ref, f)
+            if not np.array_equal(a, b):
+                bad = np.flatnonzero(a != b)
+                raise AssertionError(f"{label} {f}: {bad.size} mismatches, first at {bad[0]}")
     assert host.t == pytest.approx(STEPS * TAU, rel=0, abs=1e-12)
 
     # diagnostics: the device's fused record reduction vs exact sums
