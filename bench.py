@@ -201,6 +201,20 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def all_ranks(flag: bool, world: int) -> bool:
+    """A decision every rank takes together (what follows is collective):
+    true only if it holds on every rank -- e.g. host memory, which the
+    ranks of one node check while the others are allocating."""
+    if world == 1:
+        return flag
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def weak_n(base: int, gpus: int) -> int:
     """Grid edge with ~base^3 points per GPU: base * cbrt(G) rounded to a
     multiple of 128 (the march kernel's tile) that G divides -- exact for
@@ -379,7 +393,7 @@ def run_ours(args):
     local_bytes = 32 * g.M // max(world, 1)
     t_in = time.perf_counter()
     host = None
-    if host_memory_ok(local_bytes, L):
+    if all_ranks(host_memory_ok(local_bytes, L), world):
         host = host_preset(g, L, pinned=not args.no_e2e)
         dev = kgs.DeviceFieldState.from_host(host, g, ex)
         inputs = "host preset (block-parallel numpy, bitwise reference scenarios.py:69-89)"
@@ -492,7 +506,7 @@ def run_ours(args):
                        "wavefront, finished chunks stream out); one untimed warm-up call first"}
         # the same call on ordinary (pageable) numpy arrays -- what a dpavf
         # user passes (grid.py:82-103): page-locked just in time inside the call
-        if host_memory_ok(2 * local_bytes, L):
+        if all_ranks(host_memory_ok(2 * local_bytes, L), world):
             plain = kgs.FieldState(*(np.array(getattr(host, f)) for f in "PQUV"), host.t)
             # untimed warm-up call: allocates the page-locked staging slots
             kgs.integrate(plain, g, sc.params, sch, ex, TAU, W * TAU, record_stride=W)

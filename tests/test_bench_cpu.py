@@ -61,3 +61,35 @@ def test_bench_without_gpus_exits_nonzero():
                         "--no-e2e", "--no-cpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode != 0
     assert "CUDA devices visible" in (r.stderr + r.stdout)
+
+
+def _agree_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        q.put((rank, bench.all_ranks(rank != 1, world), bench.all_ranks(True, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_collective_decisions_agree_over_ranks():
+    """bench.all_ranks: a decision that gates collective work (host memory
+    for the e2e inputs) holds on every rank or on none."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == [False] * 3 and [r[2] for r in res] == [True] * 3
