@@ -289,15 +289,15 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
   const int64_t need = (nrec + 1) * 2 * region;
   // pageable arrays (the reference's numpy FieldState): staged through
-  // page-locked slots by host threads -- one slab's pipeline; several slabs
-  // take the plain path for them.  Page-locked arrays (FieldState.pinned) go direct.
+  // page-locked slots by host threads (one ring of slots for all slabs);
+  // page-locked arrays (FieldState.pinned) go direct.
   bool staged = false;
   if (ctx->tune_stage)
     for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
   // eligibility and buffers; the ranks of a torchrun job then agree, so all
   // of them run the pipeline (with its exchanges) or none does
   auto prepare = [&]() -> int {
-    if (!ctx->tune_pipe || ctx->d != 3 || nb < 4 || (staged && ns > 1)) return kPipeFallback;
+    if (!ctx->tune_pipe || ctx->d != 3 || nb < 4) return kPipeFallback;
     for (const Slab& s : ctx->slabs)
       if (s.nx != N) return kPipeFallback;
     if (need > (int64_t)1 << 27) return kPipeFallback;         // > 1 GiB of partials per slab
@@ -404,9 +404,22 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
 
   Slab& s0 = ctx->slabs[0];
   if (staged && ensure_host_slots(ctx, s0, stage) != KGS_OK) staged = false;
+  if (staged)   // slot events of every slab, on its own device (slab 0's come with the slots)
+    for (Slab& s : ctx->slabs) {
+      CK(cudaSetDevice(s.dev));
+      while ((int)s.hslot_ev.size() < kUpSlots + kDnSlots) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s.hslot_ev.push_back(e);
+      }
+    }
   // host threads per direction (uploads and downloads copy concurrently)
   const int cp_threads = std::max(1, std::min(8, ((int)std::thread::hardware_concurrency() - 2) / 2));
-  auto up_slot = [&](int64_t m) { return s0.hslot + (m % kUpSlots) * stage; };
+  auto up_slot = [&](int64_t u) { return s0.hslot + (u % kUpSlots) * stage; };
+  // upload slot uses in issue order (chunk-major, slab-minor) and, per slot,
+  // the event of its last DMA (on that slab's upload stream)
+  int64_t up_idx = 0;
+  cudaEvent_t last_up[kUpSlots] = {};
   // KGS_PIPE_DEBUG=1: host-side time breakdown of a staged call on stderr
   static const bool dbg = std::getenv("KGS_PIPE_DEBUG") != nullptr;
   using clk = std::chrono::steady_clock;
@@ -434,11 +447,12 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
     const size_t bytes = (size_t)nxc * nat_plane * 8;
     CK(cudaSetDevice(s.dev));
     if (staged) {
-      cudaEvent_t done = s.hslot_ev[m % kUpSlots];
+      const int64_t u = up_idx++;
+      const int k = (int)(u % kUpSlots);
       const clk::time_point t0 = clk::now();
-      if (m >= kUpSlots) CK(cudaEventSynchronize(done));   // the slot's last DMA has read it
+      if (last_up[k]) CK(cudaEventSynchronize(last_up[k]));   // the slot's last DMA has read it
       const clk::time_point t1 = clk::now();
-      double* sl = up_slot(m);
+      double* sl = up_slot(u);
       for (int f = 0; f < 4; ++f)
         par_copy((char*)(sl + f * C * nat_plane), (const char*)(host[f] + gx * nat_plane), bytes,
                  cp_threads);
@@ -447,7 +461,8 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       for (int f = 0; f < 4; ++f)
         CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, sl + f * C * nat_plane, bytes,
                            cudaMemcpyHostToDevice, s.ustream));
-      CK(cudaEventRecord(done, s.ustream));
+      CK(cudaEventRecord(s.hslot_ev[k], s.ustream));
+      last_up[k] = s.hslot_ev[k];
     } else {
       for (int f = 0; f < 4; ++f)
         CK(cudaMemcpyAsync(s.pipe_up + f * C * nat_plane, host[f] + gx * nat_plane, bytes,
@@ -478,7 +493,7 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   std::condition_variable cv;
   int64_t arrived = 0;          // chunks whose arrival event is recorded
   int err = KGS_OK;             // first error of a helper thread
-  struct DlJob { int64_t b0, nxc, j; };
+  struct DlJob { int64_t b0, nxc, j; int si; };
   std::vector<DlJob> dl_queue;  // download slot jobs, in issue order
   size_t dl_next = 0;           // next job for the downloader
   int64_t dl_done = 0;          // jobs whose host copy finished
@@ -489,7 +504,9 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       cudaSetDevice(s0.dev);
       for (const PipeEvent& e : plan) {
         if (e.kind != PIPE_ARRIVE) continue;
-        const int rc = upload_chunk(s0, e);
+        int rc = KGS_OK;
+        for (Slab& s : ctx->slabs)
+          if (!rc) rc = upload_chunk(s, e);
         {
           std::lock_guard<std::mutex> lk(mu);
           if (rc && !err) err = rc;
@@ -510,13 +527,14 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
           jb = dl_queue[dl_next++];
         }
         const clk::time_point t0 = clk::now();
-        int rc = cudaEventSynchronize(s0.hslot_ev[kUpSlots + jb.j % kDnSlots]) == cudaSuccess
+        const Slab& sj = ctx->slabs[jb.si];
+        int rc = cudaEventSynchronize(sj.hslot_ev[kUpSlots + jb.j % kDnSlots]) == cudaSuccess
                      ? KGS_OK : fail(ctx, KGS_ECUDA, "download slot event failed");
         const clk::time_point t1 = clk::now();
         if (!rc) {
           const double* sl = dn_slot(jb.j);
           for (int f = 0; f < 4; ++f)
-            par_copy((char*)(host[f] + (s0.x0 - hx0 + jb.b0) * nat_plane),
+            par_copy((char*)(host[f] + (sj.x0 - hx0 + jb.b0) * nat_plane),
                      (const char*)(sl + f * C * nat_plane), (size_t)jb.nxc * nat_plane * 8,
                      cp_threads);
         }
@@ -557,7 +575,8 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
 
   // the wavefront on the compute streams (every slab in step); face
   // exchanges between the passes; downloads behind it
-  int64_t ndl = 0;
+  int64_t ndl = 0;   // blocks copied back
+  int64_t jdl = 0;   // download slot jobs (block x slab, staged)
   for (const PipeEvent& e : plan) {
     if (r) break;
     if (e.kind == PIPE_ARRIVE) {
@@ -583,17 +602,19 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
       for (int si = 0; si < ns && !r; ++si) r = launch_range(si, passes[e.pass], e.a, e.b);
     } else {
       const int64_t k = e.pass, b0 = e.a, nxc = e.b - e.a;
-      const int64_t j = ndl++;
+      ++ndl;
       const int64_t cnt = nxc * ctx->ny * ctx->nk;
       const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->nsm * 16);
-      if (staged) {   // the download slot must have been emptied by the downloader
-        const clk::time_point t0 = clk::now();
-        std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return dl_done >= j - kDnSlots + 1 || err != KGS_OK; });
-        main_wait_dn += secs(t0, clk::now());
-        if (err) return err;
-      }
-      for (Slab& s : ctx->slabs) {
+      for (int si = 0; si < ns; ++si) {
+        Slab& s = ctx->slabs[si];
+        const int64_t j = staged ? jdl++ : 0;
+        if (staged) {   // the download slot must have been emptied by the downloader
+          const clk::time_point t0 = clk::now();
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return dl_done >= j - kDnSlots + 1 || err != KGS_OK; });
+          main_wait_dn += secs(t0, clk::now());
+          if (err) return err;
+        }
         CK(cudaSetDevice(s.dev));
         cudaEvent_t ev = s.pipe_ev[nb + k];
         CK(cudaEventRecord(ev, s.stream));
@@ -611,21 +632,21 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
                              cudaMemcpyDeviceToHost, s.dstream));
         }
         CK(cudaGetLastError());
-      }
-      if (staged) {
-        CK(cudaEventRecord(s0.hslot_ev[kUpSlots + j % kDnSlots], s0.dstream));
-        {
-          std::lock_guard<std::mutex> lk(mu);
-          dl_queue.push_back({b0, nxc, j});
+        if (staged) {
+          CK(cudaEventRecord(s.hslot_ev[kUpSlots + j % kDnSlots], s.dstream));
+          {
+            std::lock_guard<std::mutex> lk(mu);
+            dl_queue.push_back({b0, nxc, j, si});
+          }
+          cv.notify_all();
         }
-        cv.notify_all();
       }
     }
   }
   if (staged && !r) {   // every block copied out of its slot
     const clk::time_point t0 = clk::now();
     std::unique_lock<std::mutex> lk(mu);
-    cv.wait(lk, [&] { return dl_done >= ndl || err != KGS_OK; });
+    cv.wait(lk, [&] { return dl_done >= jdl || err != KGS_OK; });
     if (dbg)
       std::fprintf(stderr, "[kgs pipe] staged call %.3f s: uploader wait %.3f copy %.3f | "
                    "downloader wait %.3f copy %.3f | main wait up %.3f dn %.3f tail %.3f\n",

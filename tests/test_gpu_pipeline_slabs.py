@@ -127,3 +127,36 @@ def test_rank_pipeline_nonfinite_agrees_and_replays(monkeypatch):
         out[key] = (s, str(ei.value))
     assert_bitwise(out["rank"][0], out["one"][0], equal_nan=True)
     assert out["rank"][1] == out["one"][1]
+
+
+@pytest.mark.parametrize("slabs,N,steps,stride,planes,poison", [
+    (2, 128, 5, 1, 8, None), (4, 128, 3, 3, 4, None), (2, 256, 4, 2, 16, None),
+    (2, 128, 6, 1, 8, 64 * 128 * 128 + 11)])
+def test_slab_pipeline_pageable_arrays(slabs, N, steps, stride, planes, poison):
+    """Ordinary (pageable) numpy arrays on several slabs: staged through one
+    ring of page-locked slots by the helper threads; bitwise one slab's."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(N)
+    s0 = sc.state(g)
+    if poison is not None:
+        s0.V[poison] = np.inf
+    out = {}
+    for key, ex in (("slabs", kgs.CudaExecutor((0,), slabs_per_device=slabs)), ("one", None)):
+        ctx = get_context(g, ex)
+        ctx.set_param("pipeline_planes", planes)
+        s = s0.copy()                     # pageable
+        n0 = ctx.launch_count()
+        try:
+            tr = kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), ex, 0.01,
+                               steps * 0.01, record_stride=stride)
+            out[key] = (s, tr.energy, None, ctx.launch_count() - n0)
+        except FloatingPointError as e:
+            out[key] = (s, None, str(e), ctx.launch_count() - n0)
+        ctx.set_param("pipeline_planes", 32)
+        kgs.clear_contexts()
+    (a, ea, xa, na), (b, eb, xb, _) = out["slabs"], out["one"]
+    assert na > 40, "the pipelined path did not run"
+    assert xa == xb
+    assert_bitwise(a, b, equal_nan=True)
+    if ea is not None:
+        np.testing.assert_allclose(ea, eb, rtol=1e-13, atol=0)
