@@ -156,15 +156,21 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
  * upload P, Q, U, V, record the initial energy terms (terms0[8]), run
  * `nsteps` DP-AVF2 steps recording every `record_stride` steps into
  * terms_out[nrec][8] as kgs_step_dpavf2 does, and write the final state back
- * into the same host arrays.  On one slab the upload, the colour passes and
- * the download are overlapped as a pipeline (chunks of planes arrive around
- * plane 0; every pass advances one plane behind its predecessor; finished
- * chunks are copied back while later ones still compute -- page-locked host
- * arrays give the overlap); otherwise, or without memory for the pipeline,
- * the same result is produced by upload + kgs_step_dpavf2 + download.
- * Fields are bitwise the same either way.  KGS_ENONFINITE: the host arrays
- * hold the state after step *first_bad_step (replayed exactly), like the
- * reference's integrate.  Knobs: "pipeline" (1/0), "pipeline_planes". */
+ * into the same host arrays (this context's planes, kgs_upload's convention).
+ * The upload, the colour passes and the download are overlapped as a
+ * pipeline (chunks of planes arrive around plane 0; every pass advances one
+ * plane behind its predecessor; finished chunks are copied back while later
+ * ones still compute), on every slab side by side with the faces exchanged
+ * between the passes (kgs_pipeline_plan, split = 1); pageable arrays are
+ * staged through page-locked slots by helper threads.  The ranks of a
+ * torchrun job (kgs_create_dist) agree through NCCL on running the pipeline
+ * and on the first bad step -- every rank must make this call; terms0 /
+ * terms_out are then this rank's sums.  Without memory for the pipeline (or
+ * knob "pipeline" = 0) the same result comes from upload + kgs_step_dpavf2
+ * + download.  Fields are bitwise the same either way.  KGS_ENONFINITE: the
+ * host arrays hold the state after step *first_bad_step (replayed exactly),
+ * like the reference's integrate.  Knobs: "pipeline" (1/0),
+ * "pipeline_planes", "stage_pageable" (1/0). */
 int kgs_integrate_host(kgs_ctx* ctx, double* P, double* Q, double* U, double* V,
                        const kgs_coeffs* half, int64_t nsteps, int64_t step_offset,
                        int64_t record_stride, double* terms0, double* terms_out,
