@@ -273,7 +273,11 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
  * several slabs per GPU and inside kgs_integrate_host; 0: free-running),
  * "march_sync" (planes between cluster barriers of the
  * clustered variants), "blocks_per_sm", "march_sms" (SMs the march grid
- * spans; 0 = all), "fused_step" (1: one fused march
+ * spans; 0 = all), "record_form" (3-D record passes, the red colour's
+ * gradient terms: 2 = sums of squares of the neighbour values the update
+ * loads, completed with the new value -- the default, fastest; 1 = from the
+ * differences to the pre-update value, free of cancellation for fields with
+ * a large offset; records only, fields identical), "fused_step" (1: one fused march
  * per DP-AVF2 step -- K3 and K4 with ping-pong buffer sets, allocated on
  * first use; 3-D, rows % 16 == 0, slots % 32 == 0 -- bitwise equal but
  * currently slower; 0, the default: two colour passes), "fused_planes"

@@ -129,6 +129,7 @@ struct kgs_ctx {
   int grid_cap = 0;  // max persistent grid (blocks), sizes partials
   // tuning knobs (kgs_set_tuning): rows per tile, band height, blocks/SM cap
   int tune_ty = 4, tune_band_rows = 64, tune_occ = 0;
+  int tune_gform = 2;  // record passes: gradient-term form (2 fast, 1 cancellation-free)
   int tune_sms = 0;  // march kernel: SMs its persistent grid spans (0: all)
   int tune_xc = 0;  // march kernel planes per unit (0 auto, < 0 disables it)
   int tune_variant = 4;  // march kernel variant (kgs_launch.cuh; MV4: 8 x 64 tiles, 2 rows per thread)

@@ -785,6 +785,11 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "march_planes") ctx->tune_xc = value;
   else if (n == "blocks_per_sm") ctx->tune_occ = value;
   else if (n == "march_sms") ctx->tune_sms = value;
+  else if (n == "record_form") {
+    if (value != 1 && value != 2)
+      return fail(ctx, KGS_EINVAL, "record_form must be 1 (differences) or 2 (sums of squares)");
+    ctx->tune_gform = value;
+  }
   else if (n == "fused_step") {
 #ifndef KGS_EXPERIMENTAL
     if (value) return fail(ctx, KGS_EINVAL, "fused_step needs a -DKGS_EXPERIMENTAL build");

@@ -197,7 +197,8 @@ int make_tensor_maps(kgs_ctx* ctx, Slab& s) {
   return r;
 }
 
-template <typename Var, int COL, int OP1, int OP2, bool DIAG, bool CHECK, int DBG = 0>
+template <typename Var, int COL, int OP1, int OP2, bool DIAG, bool CHECK, int DBG = 0,
+          int GF = 2>
 int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
                  int v) {
   using L = typename Var::L;
@@ -207,7 +208,7 @@ int launch_march(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int 
   // two-rows-per-thread variants already run few, wide blocks and keep them
   constexpr int kMinB = (DIAG && Var::RPT == 1) ? (Var::MINB > 1 ? Var::MINB / 2 : 1) : Var::MINB;
   auto kern = march_pass<COL, OP1, OP2, DIAG, CHECK, Var::TY, Var::TK, Var::NOTH, Var::NOWN,
-                         kMinB, DBG, CL, Var::PW, Var::RPT>;
+                         kMinB, DBG, CL, Var::PW, Var::RPT, GF>;
   // resident CTAs per SM (or clusters per GPU / nsm when CL > 1), per device
   static int occ_dev[kMaxDevices] = {};
   static int max_clusters_dev[kMaxDevices] = {};
@@ -356,12 +357,12 @@ int march_variant(const kgs_ctx* ctx, const Slab& s, const PassGeom& g) {
   return -1;
 }
 
-template <int COL, int O1, int O2, bool DG, bool CH>
-int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
-                     int v) {
+template <int COL, int O1, int O2, bool DG, bool CH, int GF>
+int launch_march_gf(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
+                    int v) {
   switch (v) {
 #define KGS_MV_CASE(N) \
-    case N: return launch_march<MV##N, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    case N: return launch_march<MV##N, COL, O1, O2, DG, CH, 0, GF>(ctx, s, g, c, step_no, v);
     KGS_MV_CASE(0) KGS_MV_CASE(1)
 #ifdef KGS_EXPERIMENTAL
     KGS_MV_CASE(2) KGS_MV_CASE(3) KGS_MV_CASE(5) KGS_MV_CASE(6) KGS_MV_CASE(7) KGS_MV_CASE(8)
@@ -369,8 +370,19 @@ int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, 
     KGS_MV_CASE(14) KGS_MV_CASE(15)
 #endif
 #undef KGS_MV_CASE
-    default: return launch_march<MV4, COL, O1, O2, DG, CH>(ctx, s, g, c, step_no, v);
+    default: return launch_march<MV4, COL, O1, O2, DG, CH, 0, GF>(ctx, s, g, c, step_no, v);
   }
+}
+
+template <int COL, int O1, int O2, bool DG, bool CH>
+int launch_march_any(kgs_ctx* ctx, Slab& s, const PassGeom& g, const Coeffs& c, int step_no,
+                     int v) {
+  // record passes of the red colour: the gradient-term form (knob record_form)
+  if constexpr (DG && COL == 1) {
+    if (ctx->tune_gform == 1)
+      return launch_march_gf<COL, O1, O2, DG, CH, 1>(ctx, s, g, c, step_no, v);
+  }
+  return launch_march_gf<COL, O1, O2, DG, CH, 2>(ctx, s, g, c, step_no, v);
 }
 
 template <int D, int COL>

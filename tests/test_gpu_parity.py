@@ -511,3 +511,47 @@ def test_fused_halo_stores_match_copy_exchange(N, slabs):
     orc = oracle.CheckerboardOracle(3, N)
     orc.step_dpavf2(ref, args, 7, workers=oracle.CheckerboardOracle.max_threads())
     assert_bitwise(outs[1][0], ref)
+
+
+@pytest.mark.parametrize("offset", [0.0, 40.0])
+def test_record_forms_match_the_oracle(offset):
+    """Both gradient-term forms of the record passes (knob record_form: 2 =
+    sums of squares of the loaded neighbours, the default; 1 = differences
+    to the pre-update value, cancellation-free) give the oracle's exactly
+    summed energy terms; the fields do not depend on the form.  With a
+    large constant offset on U the sum-of-squares form loses accuracy in
+    proportion to (offset / neighbour difference)^2 -- the differences form
+    does not."""
+    sc = kgs.get_scenario("ellipsoids3d")
+    g = sc.default_grid(64)
+    s0 = sc.state(g)
+    s0.U += offset
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    ref = s0.copy()
+    oracle.CheckerboardOracle(3, 64).step_dpavf2(
+        ref, oracle.kernel_args(sc.params, 0.005, g), 3,
+        workers=oracle.CheckerboardOracle.max_threads())
+    want = oracle.energy_terms(ref, g)
+    outs = {}
+    for form in (2, 1):
+        dev = kgs.DeviceFieldState.from_host(s0, g)
+        dev.ctx.set_param("record_form", form)
+        terms, bad = dev.ctx.step_dpavf2(args, 3, 0, 3)
+        assert bad == 0
+        outs[form] = (dev.to_host(), np.asarray(terms[-1]))
+        dev.close()
+    assert_bitwise(outs[1][0], outs[2][0])
+    assert_bitwise(outs[1][0], ref)
+    np.testing.assert_allclose(outs[1][1], want, rtol=1e-12, atol=1e-300)
+    rel_u = abs(outs[2][1][2] - want[2]) / want[2]          # gradient sum of U
+    assert rel_u < (1e-12 if offset == 0.0 else 1e-6), rel_u
+    np.testing.assert_allclose(np.delete(outs[2][1], 2), np.delete(want, 2),
+                               rtol=1e-12, atol=1e-300)
+
+
+def test_record_form_knob_rejects_other_values():
+    g = kgs.GridSpec(3, -1.0, 1.0, 16)
+    dev = kgs.DeviceFieldState(g)
+    with pytest.raises(ValueError, match="record_form"):
+        dev.ctx.set_param("record_form", 0)
+    dev.close()
