@@ -5,7 +5,9 @@ KGS_B200_LIB=paper_2502_09537_b200/libkgs_b200_checked.so):
   resident kernel (8^3), march passes (64^3, 1 slab), virtual slabs with
   fused halo stores (64^3, 4 slabs) and copies, the opt-in fused step
   (64^3, 1 and 2 slabs), 2-D and 1-D per-pass kernels, energy/finiteness
-  passes, upload/download transforms, on-device presets.
+  passes, upload/download transforms, on-device presets, the pipelined
+  integrate() on 1 and 2 slabs from page-locked and pageable arrays, both
+  record forms.
 """
 import sys
 from pathlib import Path
@@ -37,6 +39,21 @@ def run(d, N, slabs=1, params=()):
     dev.close()
 
 
+def run_integrate(N, slabs, pinned, planes=8):
+    g = kgs.GridSpec(3, -5.0, 5.0, N)
+    p = kgs.PhysParams(1.1, 0.9, 1.2, 0.8)
+    ex = None if slabs == 1 else kgs.CudaExecutor((0,), slabs_per_device=slabs)
+    from paper_2502_09537_b200.device import get_context
+    get_context(g, ex).set_param("pipeline_planes", planes)
+    src = kgs.get_scenario("ellipsoids3d").state(g)
+    s = kgs.FieldState.pinned(g, zero=False) if pinned else src.copy()
+    if pinned:
+        for f in "PQUV":
+            getattr(s, f)[:] = getattr(src, f)
+    kgs.integrate(s, g, p, kgs.checkerboard_schedule(g), ex, 0.01, 0.04, record_stride=1)
+    kgs.clear_contexts()
+
+
 def main():
     from paper_2502_09537_b200 import _lib
     run(3, 8)                                   # resident
@@ -52,6 +69,10 @@ def main():
     run(2, 128, 2)                              # 2-D slabs
     run(1, 8192)                                # 1-D per-pass (beyond resident size)
     run(3, 8, 1, (("resident", 0),))            # small 3-D per-pass
+    run(3, 64, 1, (("record_form", 1),))        # the cancellation-free record form
+    for slabs in (1, 2):                        # pipelined integrate()
+        for pinned in (True, False):
+            run_integrate(64, slabs, pinned)
     print("sanitize runs done")
 
 
