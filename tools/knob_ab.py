@@ -3,7 +3,7 @@
 must come out bitwise identical for every setting.
 
     python tools/knob_ab.py KNOB V0,V1[,..] [--N 1024] [--steps 6] [--reps 4] [--call]
-                            [--scenario fourpeak2d]
+                            [--scenario fourpeak2d] [--record 1]
 
 --call times the whole kgs_step_dpavf2 call (host wall clock around the
 synchronous call, one untimed warm-up call first) instead of the per-pass
@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--call", action="store_true")
     ap.add_argument("--scenario", default="ellipsoids3d")
+    ap.add_argument("--record", type=int, default=0, help="record stride (0: once at the end)")
     a = ap.parse_args()
     vals = [int(v) for v in a.values.split(",")]
     sc = kgs.get_scenario(a.scenario)
@@ -43,7 +44,7 @@ def main():
             if a.call:
                 dev.ctx.step_dpavf2(args, 2, 0, 2)
                 t0 = time.perf_counter()
-                dev.ctx.step_dpavf2(args, a.steps, 0, a.steps)
+                dev.ctx.step_dpavf2(args, a.steps, 0, a.record or a.steps)
                 times[v].append((time.perf_counter() - t0) * 1e3 / a.steps)
             else:
                 dev.ctx.pass_timing(True)
