@@ -76,6 +76,16 @@ struct Slab {
 #endif
   double* partials[2] = {nullptr, nullptr};  // per colour pass, grid * NTERMS
   int npart[2] = {0, 0};                     // blocks that wrote partials
+  // record reductions run on their own stream (fstream), off the passes'
+  // critical path: the partials are double-buffered per record (the set not
+  // in use is partials_alt); fin_busy[s]: a reduction still reads set s,
+  // done at ev_fin[s]; pset = the set `partials` points at
+  double* partials_alt[2] = {nullptr, nullptr};
+  cudaStream_t fstream = nullptr;
+  cudaEvent_t ev_fin[2] = {nullptr, nullptr};
+  cudaEvent_t ev_diag = nullptr;
+  bool fin_busy[2] = {false, false};
+  int pset = 0;
   double* records = nullptr;                 // device [cap * NTERMS]
   int64_t rec_cap = 0;
   unsigned long long* bad = nullptr;

@@ -178,7 +178,14 @@ int step_fused(kgs_ctx* ctx, bool rec, bool last, const Coeffs& c, int step_no) 
       CK(cudaStreamWaitEvent(s.stream, ctx->slabs[(i - 1 + ns) % ns].ev_face[(k - 1) & 1], 0));
       CK(cudaStreamWaitEvent(s.stream, ctx->slabs[(i + 1) % ns].ev_face[(k - 1) & 1], 0));
     }
-    if (rec) { s.npart[1] = 0; s.npart[0] = 0; }
+    if (rec) {
+      s.npart[1] = 0;
+      s.npart[0] = 0;
+      if (s.fin_busy[s.pset]) {   // a record reduction still reads this partial set
+        CK(cudaStreamWaitEvent(s.stream, s.ev_fin[s.pset], 0));
+        s.fin_busy[s.pset] = false;
+      }
+    }
     const int xa = multi ? 1 : 0, xb = multi ? s.nx - 1 : s.nx;
     int r;
     if (rec) r = last ? launch_step<true, OP_NONE>(ctx, s, c, step_no, xa, xb)

@@ -193,10 +193,16 @@ int kgs_destroy(kgs_ctx* ctx) {
   for (auto& s : ctx->slabs) {
     cudaSetDevice(s.dev);
     if (s.stream) cudaStreamSynchronize(s.stream);
+    if (s.fstream) cudaStreamSynchronize(s.fstream);
     for (int c = 0; c < 2; ++c) {
       if (s.buf[c]) cudaFree(s.buf[c]);
       if (s.partials[c]) cudaFree(s.partials[c]);
+      if (s.partials_alt[c]) cudaFree(s.partials_alt[c]);
     }
+    for (int i = 0; i < 2; ++i)
+      if (s.ev_fin[i]) cudaEventDestroy(s.ev_fin[i]);
+    if (s.ev_diag) cudaEventDestroy(s.ev_diag);
+    if (s.fstream) cudaStreamDestroy(s.fstream);
     if (s.records) cudaFree(s.records);
     if (s.bad) cudaFree(s.bad);
     if (s.wctr) cudaFree(s.wctr);
@@ -442,6 +448,9 @@ int kgs_step_dpavf2(kgs_ctx* ctx, const kgs_coeffs* half, int64_t nsteps,
     CK(cudaSetDevice(s.dev));
     // the step ends when the last halo exchange has landed
     if (s.xch_pending) CK(cudaStreamWaitEvent(s.stream, s.ev_xch, 0));
+    // ... and its record reductions (record stream) are done
+    for (int i = 0; i < 2; ++i)
+      if (s.fin_busy[i]) CK(cudaStreamWaitEvent(s.stream, s.ev_fin[i], 0));
     CK(cudaEventRecord(s.ev_t1, s.stream));
   }
   r = sync_all(ctx);

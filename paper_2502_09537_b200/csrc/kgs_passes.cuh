@@ -101,6 +101,8 @@ int sync_all(kgs_ctx* ctx) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamSynchronize(s.stream));
     CK(cudaStreamSynchronize(s.cstream));
+    CK(cudaStreamSynchronize(s.fstream));
+    s.fin_busy[0] = s.fin_busy[1] = false;
   }
   return KGS_OK;
 }
@@ -138,7 +140,14 @@ int run_program(kgs_ctx* ctx, const Program& prog, const Coeffs& c) {
         if (split) ctx->pass_no++;
         int64_t pts = 0;
         for (auto& s : ctx->slabs) {
-          if (o.diag) s.npart[o.col] = 0;
+          if (o.diag) {
+            s.npart[o.col] = 0;
+            if (s.fin_busy[s.pset]) {   // a record reduction still reads this set
+              CK(cudaSetDevice(s.dev));
+              CK(cudaStreamWaitEvent(s.stream, s.ev_fin[s.pset], 0));
+              s.fin_busy[s.pset] = false;
+            }
+          }
           pts += (int64_t)s.nx * ctx->ny * ctx->nk;
         }
         timing = o.xa && ctx->pass_timing;
@@ -279,13 +288,24 @@ int collect_pass_times(kgs_ctx* ctx) {
   return KGS_OK;
 }
 
+// Reduce the current partial set into record `slot` on the slab's record
+// stream, after the passes that wrote it, and switch the passes to the other
+// set: the next steps' passes do not wait for the reduction (the set is
+// only written again two records later, after waiting for ev_fin).
 int finalize_record(kgs_ctx* ctx, int64_t slot, bool both) {
   for (auto& s : ctx->slabs) {
     CK(cudaSetDevice(s.dev));
-    CK(launch_dependent(ctx->tune_pdl != 0, finalize_terms, 1u, (unsigned)kThreads, 0, s.stream,
-                        (const double*)s.partials[1], s.npart[1],
-                        (const double*)(both ? s.partials[0] : nullptr), both ? s.npart[0] : 0,
-                        s.records + slot * NTERMS));
+    CK(cudaEventRecord(s.ev_diag, s.stream));
+    CK(cudaStreamWaitEvent(s.fstream, s.ev_diag, 0));
+    finalize_terms<<<1, kThreads, 0, s.fstream>>>(
+        (const double*)s.partials[1], s.npart[1], (const double*)(both ? s.partials[0] : nullptr),
+        both ? s.npart[0] : 0, s.records + slot * NTERMS);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s.ev_fin[s.pset], s.fstream));
+    s.fin_busy[s.pset] = true;
+    std::swap(s.partials[0], s.partials_alt[0]);
+    std::swap(s.partials[1], s.partials_alt[1]);
+    s.pset ^= 1;
     ctx->launches++;
   }
   return KGS_OK;
@@ -356,6 +376,7 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
     s.plane0[c] = s.buf[c] + ctx->ps;
     // up to 3 launches (interior + 2 boundary planes) per pass write partials
     CK(cudaMalloc(&s.partials[c], (size_t)4 * ctx->grid_cap * NTERMS * sizeof(double)));
+    CK(cudaMalloc(&s.partials_alt[c], (size_t)4 * ctx->grid_cap * NTERMS * sizeof(double)));
   }
   if (ctx->d == 3) {
     int r = make_tensor_maps(ctx, s);
@@ -373,6 +394,9 @@ int alloc_slab(kgs_ctx* ctx, Slab& s) {
   CK(cudaMalloc(&s.stage, s.stage_planes * nat_plane));
   CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&s.cstream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s.fstream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&s.ev_fin[i], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s.ev_diag, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_bnd, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_xch, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i)

@@ -3,7 +3,7 @@ each repetition runs one fresh process per library (selected with
 KGS_B200_LIB) that times a whole kgs_step_dpavf2 call after a warm-up call;
 the fields must come out bitwise identical for every library.
 
-    python tools/lib_ab.py LIB_A LIB_B [--N 1024] [--steps 20] [--reps 3] [--record 1]
+    python tools/lib_ab.py LIB_A LIB_B [--N 1024] [--steps 20] [--reps 3] [--record 1] [--scenario fourpeak2d]
 """
 import argparse
 import json
@@ -18,11 +18,11 @@ CHILD = r"""
 import hashlib, json, sys, time
 sys.path.insert(0, %r)
 import paper_2502_09537_b200 as kgs
-N, steps, rec = %d, %d, %d
-sc = kgs.get_scenario("ellipsoids3d")
+N, steps, rec, scen = %d, %d, %d, %r
+sc = kgs.get_scenario(scen)
 g = sc.default_grid(N)
 args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
-dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
+dev = kgs.DeviceFieldState.from_preset(scen, g)
 dev.ctx.step_dpavf2(args, 2, 0, 2)
 t0 = time.perf_counter()
 terms, _ = dev.ctx.step_dpavf2(args, steps, 0, rec or steps)
@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--N", type=int, default=1024)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--scenario", default="ellipsoids3d")
     ap.add_argument("--record", type=int, default=0, help="record stride of the timed call (0: once at its end)")
     a = ap.parse_args()
     res = {lib: [] for lib in a.libs}
@@ -49,7 +50,7 @@ def main():
     for _ in range(a.reps):
         for lib in a.libs:
             env = dict(os.environ, KGS_B200_LIB=str(Path(lib).resolve()))
-            out = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), a.N, a.steps, a.record)],
+            out = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), a.N, a.steps, a.record, a.scenario)],
                                  env=env, capture_output=True, text=True, check=True).stdout
             r = json.loads(out.strip().splitlines()[-1])
             res[lib].append(round(r["step_ms"], 4))
@@ -58,7 +59,7 @@ def main():
     out = {lib: {"step_ms": v, "mean": round(sum(v) / len(v), 4)} for lib, v in res.items()}
     t0 = terms[a.libs[0]]
     rel = {lib: max(abs(x - y) / max(abs(y), 1e-300) for x, y in zip(t, t0)) for lib, t in terms.items()}
-    print(json.dumps({"N": a.N, **out, "bitwise_equal": len(set(digests.values())) == 1,
+    print(json.dumps({"N": a.N, "scenario": a.scenario, **out, "bitwise_equal": len(set(digests.values())) == 1,
                       "terms_max_rel_vs_first": rel}))
 
 
