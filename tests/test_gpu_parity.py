@@ -466,6 +466,30 @@ def test_resident_kernel_matches_passes_and_reference(golden, name):
     assert_bitwise(outs[1][0], ref)
 
 
+@pytest.mark.parametrize("scenario,N,steps,stride", [
+    ("soliton1d", 1024, 37, 1), ("soliton1d", 1024, 16, 1), ("fourpeak2d", 64, 29, 3),
+    ("ellipsoids3d", 16, 9, 1)])
+def test_resident_record_batches(scenario, N, steps, stride):
+    """The resident kernel stores its records in batches of 8 (per-warp sums,
+    one block sum per batch): full and partial batches, strides > 1 -- the
+    records equal the per-pass path's to reduction order and the fields
+    stay bitwise."""
+    sc = kgs.get_scenario(scenario)
+    g = sc.default_grid(N)
+    args = kgs.precompute_coefficients(sc.params, 0.005, g).kernel_args()
+    outs = []
+    for resident in (0, 1):
+        dev = kgs.DeviceFieldState.from_preset(scenario, g)
+        dev.ctx.set_param("resident", resident)
+        terms, bad = dev.ctx.step_dpavf2(args, steps, 0, stride)
+        assert bad == 0
+        outs.append((dev.to_host(), np.asarray(terms)))
+        dev.close()
+    assert outs[1][1].shape == (steps // stride, 8)
+    assert_bitwise(outs[0][0], outs[1][0])
+    np.testing.assert_allclose(outs[1][1], outs[0][1], rtol=1e-13, atol=1e-300)
+
+
 def test_oversized_grid_fails_cleanly_and_device_stays_usable():
     """2048^3 (275 GB) does not fit one B200: MemoryError naming the
     allocation, nothing leaked -- a normal context works right after."""
