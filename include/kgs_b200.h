@@ -292,10 +292,12 @@ int kgs_set_tuning(kgs_ctx* ctx, int rows_per_tile, int band_rows, int blocks_pe
  * kernel's own-tile write: 0 per-thread stores, 1 one TMA bulk store, 2,
  * the default, bulk store with an L2 evict-first hint), "pipeline" (1, the
  * default: kgs_integrate_host overlaps upload, passes and download on one
- * slab; 0: in sequence), "pipeline_planes" (its chunk, default 32 planes),
- * "pdl" (1, the default: the colour passes and record reductions are
- * launched as programmatic dependents of the previous kernel on the stream,
- * so their launch and set-up overlap its drain; 0: plain stream order).
+ * slab; 0: in sequence), "pipeline_planes" (its chunk in planes; 0, the
+ * default: 16 for page-locked arrays when the per-record partials fit,
+ * else 32), "pdl" (1, the default: the colour passes are launched as
+ * programmatic dependents of the previous kernel on the stream, so their
+ * launch and set-up overlap its drain; 0: plain stream order; record
+ * reductions run on a per-slab record stream either way).
  * KGS_EINVAL for unknown names. */
 int kgs_set_param(kgs_ctx* ctx, const char* name, int value);
 

@@ -158,7 +158,7 @@ struct kgs_ctx {
   int tune_tstore = 2;
   int tune_pdl = 1;          // colour passes: programmatic dependent launch
   int tune_pipe = 1;         // kgs_integrate_host: overlap upload | passes | download
-  int tune_pipe_chunk = 32;  // planes per transfer chunk
+  int tune_pipe_chunk = 0;   // planes per transfer chunk (0: auto, 16 or 32)
   int tune_stage = 1;        // kgs_integrate_host: stage pageable host arrays via page-locked slots     // march own-tile write: 0 STG, 1 TMA bulk store, 2 + L2 evict-first
   // fused halo exchange (single-process slabs): boundary launches
   // store their faces straight into the neighbours' ghost planes

@@ -810,7 +810,7 @@ int kgs_set_param(kgs_ctx* ctx, const char* name, int value) {
   else if (n == "resident") ctx->tune_resident = value;
   else if (n == "tma_store") ctx->tune_tstore = value;
   else if (n == "pipeline") ctx->tune_pipe = value;
-  else if (n == "pipeline_planes") ctx->tune_pipe_chunk = std::max(1, value);
+  else if (n == "pipeline_planes") ctx->tune_pipe_chunk = std::max(0, value);   // 0: auto
   else if (n == "stage_pageable") ctx->tune_stage = value;
   else if (n == "mirror_halo") ctx->tune_mirror = value;
   else if (n == "pdl") ctx->tune_pdl = value;

@@ -279,8 +279,25 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   // with face exchanges between the passes (pipeline_plan)
   const bool split = needs_exchange(ctx);
   const int64_t N = ctx->slabs[0].nx;   // planes per slab
-  // chunk planes; a layout-transform launch covers < 2^31 point pairs (decode_point)
-  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(ctx->tune_pipe_chunk,
+  // pageable arrays (the reference's numpy FieldState): staged through
+  // page-locked slots by host threads (one ring of slots for all slabs);
+  // page-locked arrays (FieldState.pinned) go direct.
+  bool staged = false;
+  if (ctx->tune_stage)
+    for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
+  // doubles of per-record partials for chunks of c planes: every launch of
+  // a pass (<= chunks + 4) writes grid_cap blocks of NTERMS, per record and colour
+  auto partials_for = [&](int64_t c) {
+    return (nrec + 1) * 2 * (((N + c - 1) / c + 4) * ctx->grid_cap * NTERMS);
+  };
+  constexpr int64_t kPartMax = (int64_t)1 << 27;               // 1 GiB of partials per slab
+  // chunk planes (knob pipeline_planes; 0 = auto: 16 for page-locked arrays
+  // -- the shorter wavefront drain; 1024^3, 20 steps: 0.848 vs 0.877 s per
+  // call -- unless that many partial regions do not fit, else 32); a
+  // layout-transform launch covers < 2^31 point pairs (decode_point)
+  int64_t want = ctx->tune_pipe_chunk;
+  if (want <= 0) want = (!staged && partials_for(16) <= kPartMax) ? 16 : 32;
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(want,
                                                            ((1ll << 31) - 1) / ((int64_t)ctx->ny * ctx->nk)));
   const int64_t nb = (N + C - 1) / C;
   const int64_t nat_plane = (int64_t)ctx->ny * ctx->nz;
@@ -288,19 +305,13 @@ int integrate_pipelined(kgs_ctx* ctx, double* const host[4], const Coeffs& c, in
   const int64_t maxl = nb + 4;                                 // launches per pass
   const int64_t region = maxl * ctx->grid_cap * NTERMS;        // doubles per (record, colour)
   const int64_t need = (nrec + 1) * 2 * region;
-  // pageable arrays (the reference's numpy FieldState): staged through
-  // page-locked slots by host threads (one ring of slots for all slabs);
-  // page-locked arrays (FieldState.pinned) go direct.
-  bool staged = false;
-  if (ctx->tune_stage)
-    for (int f = 0; f < 4; ++f) staged = staged || host_pageable(host[f]);
   // eligibility and buffers; the ranks of a torchrun job then agree, so all
   // of them run the pipeline (with its exchanges) or none does
   auto prepare = [&]() -> int {
     if (!ctx->tune_pipe || ctx->d != 3 || nb < 4) return kPipeFallback;
     for (const Slab& s : ctx->slabs)
       if (s.nx != N) return kPipeFallback;
-    if (need > (int64_t)1 << 27) return kPipeFallback;         // > 1 GiB of partials per slab
+    if (need > kPartMax) return kPipeFallback;
     if (ensure_alt(ctx)) return kPipeFallback;
     for (Slab& s : ctx->slabs) {
       CK(cudaSetDevice(s.dev));

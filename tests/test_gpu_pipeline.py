@@ -23,14 +23,15 @@ def _run(g, sc, s0, tau, T, stride, pipeline, planes=32):
     tr = kgs.integrate(s, g, sc.params, kgs.checkerboard_schedule(g), None, tau, T,
                        record_stride=stride)
     ctx.set_param("pipeline", 1)
-    ctx.set_param("pipeline_planes", 32)
+    ctx.set_param("pipeline_planes", 0)
     return s, tr
 
 
 @pytest.mark.parametrize("N,steps,stride,planes", [
     (128, 5, 1, 32), (128, 7, 3, 8), (128, 4, 4, 5), (192, 3, 2, 16), (256, 6, 6, 32),
     (128, 1, 1, 32), (64, 9, 2, 4), (128, 1, 1, 3), (128, 2, 1, 6), (128, 3, 3, 7),
-    (128, 20, 5, 32), (512, 10, 5, 32)])
+    (128, 20, 5, 32), (512, 10, 5, 32),
+    (128, 5, 1, 0), (256, 6, 1, 0), (512, 10, 5, 0)])   # 0: the auto chunk (16 here)
 def test_pipeline_bitwise_vs_plain_and_oracle(N, steps, stride, planes):
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(N)
@@ -172,7 +173,7 @@ def test_pipeline_with_pinned_host_arrays(N, steps, stride, planes, poison):
             res = (None, str(e))
         outs.append((s.copy(), res))
     ctx.set_param("pipeline", 1)
-    ctx.set_param("pipeline_planes", 32)
+    ctx.set_param("pipeline_planes", 0)
     (a, (ea, xa)), (b, (eb, xb)) = outs
     assert xa == xb
     assert_bitwise(a, b, equal_nan=True)
@@ -207,7 +208,7 @@ def test_pipeline_pageable_arrays_staged(N, steps, stride, planes, poison):
             res = (None, str(e))
         outs.append((s.copy(), res))
     ctx.set_param("stage_pageable", 1)
-    ctx.set_param("pipeline_planes", 32)
+    ctx.set_param("pipeline_planes", 0)
     a, (ea, xa) = outs[0]
     for b, (eb, xb) in outs[1:]:
         assert xa == xb

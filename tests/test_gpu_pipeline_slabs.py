@@ -42,7 +42,7 @@ def _run(g, sc, s0, ex, tau, steps, stride, pipeline, planes):
                        record_stride=stride)
     n = ctx.launch_count() - n0
     ctx.set_param("pipeline", 1)
-    ctx.set_param("pipeline_planes", 32)
+    ctx.set_param("pipeline_planes", 0)
     return s, tr, n
 
 
@@ -152,7 +152,7 @@ def test_slab_pipeline_pageable_arrays(slabs, N, steps, stride, planes, poison):
             out[key] = (s, tr.energy, None, ctx.launch_count() - n0)
         except FloatingPointError as e:
             out[key] = (s, None, str(e), ctx.launch_count() - n0)
-        ctx.set_param("pipeline_planes", 32)
+        ctx.set_param("pipeline_planes", 0)
         kgs.clear_contexts()
     (a, ea, xa, na), (b, eb, xb, _) = out["slabs"], out["one"]
     assert na > 40, "the pipelined path did not run"

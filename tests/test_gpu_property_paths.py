@@ -53,7 +53,7 @@ def test_pipeline_equals_plain(N, planes, steps, stride, seed, tau, poison, plan
         except FloatingPointError as e:
             outs.append((s.copy(), None, str(e)))
     ctx.set_param("pipeline", 1)
-    ctx.set_param("pipeline_planes", 32)
+    ctx.set_param("pipeline_planes", 0)
     (a, ea, xa), (b, eb, xb) = outs
     assert xa == xb
     for f in "PQUV":
@@ -225,7 +225,7 @@ def test_slab_pipeline_equals_one_slab(N, slabs, planes, steps, stride, seed, ta
             outs.append((s.copy(), tr.energy, None))
         except FloatingPointError as e:
             outs.append((s.copy(), None, str(e)))
-        ctx.set_param("pipeline_planes", 32)
+        ctx.set_param("pipeline_planes", 0)
     (a, ea, xa), (b, eb, xb) = outs
     assert xa == xb
     for f in "PQUV":

@@ -1,5 +1,7 @@
 """Time integrate() on a pinned host state: first (cold context) vs warm calls,
-pipeline on / off.   python tools/e2e_probe.py [N] [K]"""
+pipeline on / off, chunk sizes.   python tools/e2e_probe.py [N] [K] [--chunks 8,16,32 --reps 3]
+(--chunks: only warm pipelined calls, chunk sizes interleaved over --reps
+repetitions; median wall per chunk size)"""
 import json
 import sys
 import time
@@ -11,8 +13,10 @@ from paper_2502_09537_b200.device import get_context
 
 
 def main():
-    N = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
-    K = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+    pos = [a for i, a in enumerate(sys.argv[1:], 1)
+           if not a.startswith("--") and not sys.argv[i - 1].startswith("--")]
+    N = int(pos[0]) if len(pos) > 0 else 1024
+    K = int(pos[1]) if len(pos) > 1 else 40
     sc = kgs.get_scenario("ellipsoids3d")
     g = sc.default_grid(N)
     host = kgs.FieldState.pinned(g)
@@ -21,6 +25,24 @@ def main():
     dev.close()
     sch = kgs.checkerboard_schedule(g)
     out = {}
+    if "--chunks" in sys.argv:
+        chunks = [int(c) for c in sys.argv[sys.argv.index("--chunks") + 1].split(",")]
+        reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
+        kgs.integrate(host, g, sc.params, sch, None, 0.01, K * 0.01, record_stride=K)  # warm
+        walls = {c: [] for c in chunks}
+        for _ in range(reps):
+            for c in chunks:
+                get_context(g, None).set_param("pipeline_planes", c)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                kgs.integrate(host, g, sc.params, sch, None, 0.01, K * 0.01, record_stride=K)
+                torch.cuda.synchronize()
+                walls[c].append(round(time.perf_counter() - t0, 4))
+        for c, w in walls.items():
+            m = sorted(w)[len(w) // 2]
+            out[f"c{c}"] = {"walls_s": w, "median_s": m, "Gupd_s": round(2 * g.M * K / m / 1e9, 1)}
+        print(json.dumps({"N": N, "K": K, **out}))
+        return
     runs = [("cold_pipe", 1, 32), ("warm_pipe", 1, 32), ("warm_plain", 0, 32)]
     runs += [(f"warm_pipe_c{c}", 1, c) for c in (16, 24, 48, 64, 16, 32, 64)]
     for label, pipe, chunk in runs:
