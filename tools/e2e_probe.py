@@ -1,5 +1,5 @@
 """Time integrate() on a pinned host state: first (cold context) vs warm calls,
-pipeline on / off, chunk sizes.   python tools/e2e_probe.py [N] [K] [--chunks 8,16,32 --reps 3]
+pipeline on / off, chunk sizes.   python tools/e2e_probe.py [N] [K] [--chunks 8,16,32 --reps 3] [--pageable]
 (--chunks: only warm pipelined calls, chunk sizes interleaved over --reps
 repetitions; median wall per chunk size)"""
 import json
@@ -14,7 +14,7 @@ from paper_2502_09537_b200.device import get_context
 
 def main():
     pos = [a for i, a in enumerate(sys.argv[1:], 1)
-           if not a.startswith("--") and not sys.argv[i - 1].startswith("--")]
+           if not a.startswith("--") and sys.argv[i - 1] not in ("--chunks", "--reps")]
     N = int(pos[0]) if len(pos) > 0 else 1024
     K = int(pos[1]) if len(pos) > 1 else 40
     sc = kgs.get_scenario("ellipsoids3d")
@@ -23,6 +23,9 @@ def main():
     dev = kgs.DeviceFieldState.from_preset("ellipsoids3d", g)
     dev.download(host)
     dev.close()
+    if "--pageable" in sys.argv:   # ordinary numpy arrays (staged inside the call)
+        import numpy as np
+        host = kgs.FieldState(*(np.array(getattr(host, f)) for f in "PQUV"), host.t)
     sch = kgs.checkerboard_schedule(g)
     out = {}
     if "--chunks" in sys.argv:
